@@ -1,0 +1,152 @@
+"""Pins for oracle/solvers.py: invariants, fixed points, textbook special cases."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+import synth
+from oracle import fem, geometry as G, solvers, surrogate as S
+
+
+@pytest.fixture(scope="module")
+def shell3():
+    m = synth.shell_mesh(0.55, 1.0, 0, 1)
+    L = 3
+    num = G.Numbering(m, 2 ** L)
+    Lt, Lx, _ = S.surrogate_operator(m, L, 2, num=num)
+    return m, num, Lt, Lx
+
+
+def test_apply_annihilates_constants_away_from_boundary(shell3):
+    m, num, Lt, Lx = shell3
+    y = Lt @ np.ones(num.n_total)
+    vol = np.arange(num.base_v, num.n_total)
+    assert np.abs(y[vol]).max() < 1e-13
+    # with Dirichlet masking only rows with a Dirichlet neighbour change
+    Lm = Lt.tocsr()
+    u = num.unknown_mask.astype(float)
+    y2 = solvers.apply(Lt, num, u)
+    for g in vol[::37]:
+        cols = Lm[g].indices
+        if num.unknown_mask[cols].all():
+            assert abs(y2[g]) < 1e-13
+
+
+def test_residual_of_zero_is_rhs(shell3):
+    m, num, Lt, Lx = shell3
+    f = synth.uniform_pm1(3, np.arange(num.n_total))
+    f[num.dirichlet_mask] = 0
+    r = solvers.residual(Lt, num, np.zeros(num.n_total), f)
+    assert np.array_equal(r, f)
+
+
+def test_affine_surrogate_apply_equals_fem_apply():
+    m = synth.single_tet()
+    flat = synth.MacroMesh(m.vertices, None, m.tets, m.dirichlet)
+    L = 4
+    num = G.Numbering(flat, 2 ** L)
+    A = fem.assemble(flat, 2 ** L, num, blended=False)
+    cf = np.stack([S.fit_macro(flat, 0, L, 2, blended=False)])
+    Lt, _, _ = S.surrogate_operator(flat, L, 2, num=num, A_exact=A, coeffs=cf)
+    u = synth.uniform_pm1(0, np.arange(num.n_total))
+    assert np.abs(solvers.apply(Lt, num, u) - solvers.apply(A, num, u)).max() < 1e-13
+
+
+def test_gs_fixed_point_and_independent_volume_colours(shell3):
+    m, num, Lt, Lx = shell3
+    gs = solvers.GS(Lt, num)
+    unk = np.nonzero(num.unknown_mask)[0]
+    f = synth.uniform_pm1(1, np.arange(num.n_total))
+    f[num.dirichlet_mask] = 0
+    Lu = Lt.tocsr()[unk][:, unk]
+    ustar = np.zeros(num.n_total)
+    ustar[unk] = spla.spsolve(Lu.tocsc(), f[unk])
+    u1 = gs.sweep(ustar.copy(), f)
+    assert np.abs(u1 - ustar).max() < 1e-12 * np.abs(ustar).max()
+    for s in gs.steps[-4:]:                              # volume colours
+        sub = Lt.tocsr()[s][:, s]
+        sub = sub - sp.diags(sub.diagonal())
+        assert abs(sub).max() == 0.0
+
+
+def test_gs_matches_dense_colour_gs(shell3):
+    m, num, Lt, Lx = shell3
+    gs = solvers.GS(Lt, num)
+    D = Lt.toarray()
+    msk = num.unknown_mask
+    u0 = synth.uniform_pm1(5, np.arange(num.n_total)) * msk
+    f = synth.uniform_pm1(6, np.arange(num.n_total)) * msk
+    u = u0.copy()
+    for s in gs.steps:                                   # dense, literal eq. iteration-scheme
+        old = u.copy()
+        for I in s:
+            acc = f[I]
+            for J in np.nonzero(D[I])[0]:
+                if J != I and msk[J]:
+                    acc -= D[I, J] * old[J]
+            u[I] = acc / D[I, I]
+    assert np.abs(gs.sweep(u0.copy(), f) - u).max() < 1e-13
+
+
+def test_gs_reduces_energy_error_for_symmetric_fem(shell3):
+    m, num, Lt, Lx = shell3
+    gs = solvers.GS(Lx, num)
+    Lm = fem.apply_dirichlet(Lx, num)
+    e = synth.uniform_pm1(2, np.arange(num.n_total)) * num.unknown_mask
+    f = np.zeros(num.n_total)
+    en = [e @ (Lm @ e)]
+    for _ in range(3):
+        e = gs.sweep(e, f)
+        en.append(e @ (Lm @ e))
+    assert all(b < a for a, b in zip(en, en[1:]))
+
+
+def test_parity_rule_unique_coarse_edge_brute_force():
+    N = 8
+    lat = G.lattice_ijk(N)
+    coarse = lat[np.all(lat % 2 == 0, axis=1)]
+    cset = {tuple(c) for c in coarse}
+    for F in lat:
+        if np.all(F % 2 == 0):
+            continue
+        # exactly one coarse edge (pair of coarse nodes 2d apart along a lattice
+        # direction) has F as its midpoint, and it is the parity-class direction
+        pairs = {frozenset({tuple(F - d), tuple(F + d)}) for d in G.DIRS if np.any(d)
+                 and tuple(F - d) in cset and tuple(F + d) in cset}
+        assert len(pairs) == 1
+        d = solvers._PARITY_DIR[tuple(F % 2)]
+        assert pairs == {frozenset({tuple(F - np.array(d)), tuple(F + np.array(d))})}
+
+
+def test_prolongation_reproduces_affine_functions_and_R_is_transpose():
+    m = synth.shell_mesh(0.55, 1.0, 0, 1)
+    flat = synth.MacroMesh(m.vertices, None, m.tets, m.dirichlet)
+    nc, nf = G.Numbering(flat, 4), G.Numbering(flat, 8)
+    P = solvers.prolongation(flat, nc, nf, masked=False)
+    Xc, Xf = nc.coords(False), nf.coords(False)
+    assert np.abs(P @ Xc - Xf).max() < 1e-14
+    assert np.allclose(P @ np.ones(nc.n_total), 1.0)
+    Pm = solvers.prolongation(flat, nc, nf)
+    assert abs(Pm.T - Pm.T.tocsr()).max() == 0
+
+
+def test_cg_matches_scipy_and_vcycle_contracts():
+    m = synth.shell_mesh(0.55, 1.0, 0, 1)
+    H = solvers.Hierarchy(m, 4, 2, 2)
+    A = H.A_coarse
+    num = H.num[2]
+    b = synth.uniform_pm1(9, np.arange(num.n_total)) * num.unknown_mask
+    x = solvers.cg(A, b, 50)
+    unk = num.unknown_mask
+    ref, _ = spla.cg(A[unk][:, unk], b[unk], rtol=1e-14, atol=0, maxiter=500)
+    assert np.abs(x[unk] - ref).max() < 1e-8 * np.abs(ref).max()
+    # zero rhs + zero guess stays zero
+    z = np.zeros(H.num[4].n_total)
+    u, hist = H.solve(z.copy(), z, 1)
+    assert np.all(u == 0) and np.all(hist == 0)
+    num4 = H.num[4]
+    f = synth.uniform_pm1(4, np.arange(num4.n_total)) * num4.unknown_mask
+    u0 = synth.uniform_pm1(7, np.arange(num4.n_total)) * num4.unknown_mask
+    u, hist = H.solve(u0, f, 6)
+    rates = hist[1:] / hist[:-1]
+    assert np.all(rates[2:] < 0.5), rates
