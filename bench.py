@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Benchmark: surrogate stencil apply + multicolour GS sweep (fp64) on B200.
+
+Metric (BASELINE.json): "GLUP/s surrogate stencil apply + GS sweep (fp64) at
+1/2/4/8 B200; % HBM roofline".  One step = one surrogate apply y = L~u plus
+one full multicolour GS sweep on u (every unknown updated once by each), i.e.
+2 * n_unknowns lattice updates per step.
+
+Workload at N = 1: BASELINE config 4's per-GPU weak-scaling load -- the
+480-macro shell (t=1, n_r=2), L = 7, q = 2 LSQP (j = 2), 167,117,310 unknowns,
+inputs (1.4 GB per vector) far larger than L2.
+
+`--impl reference` times the CPU oracle (oracle/) on a bounded sample of the
+same workload on the host cores (the reference arm for this paper-only tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GLUP/s surrogate stencil apply + GS sweep (fp64) at 1/2/4/8 B200; % HBM roofline"
+UNIT = "GLUP/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--t", type=int, default=1, help="icosahedral refinements")
+    p.add_argument("--nr", type=int, default=2, help="radial layers")
+    p.add_argument("--L", type=int, default=7)
+    p.add_argument("--q", type=int, default=2)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-extras", action="store_true")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for n, v in zip(names, s[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle leg (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------
+def oracle_sample(L, q, n_macros=1):
+    """The oracle on a bounded sample of the workload: the first `n_macros`
+    macros of the same shell at the same level, as a stand-alone mesh with all
+    outer faces Dirichlet.  Returns (n_unknowns, step_fn)."""
+    import numpy as np
+
+    import synth
+    from oracle import geometry as G, solvers, surrogate as S
+    sh = synth.shell_mesh(0.55, 1.0, 1, 2)
+    tets = sh.tets[:n_macros]
+    vids = np.unique(tets)
+    remap = {int(v): i for i, v in enumerate(vids)}
+    t2 = np.vectorize(remap.get)(tets)
+    mesh = synth.MacroMesh(sh.vertices[vids], sh.radius[vids], t2, np.ones_like(t2, dtype=np.uint8))
+    num = G.Numbering(mesh, 2 ** L)
+    Lt, _, _ = S.surrogate_operator(mesh, L, q, num=num)
+    gs = solvers.GS(Lt, num)
+    g = np.arange(num.n_total)
+    u = synth.uniform_pm1(0, g) * num.unknown_mask
+    f = synth.uniform_pm1(1, g) * num.unknown_mask
+    n_unk = int(num.unknown_mask.sum())
+
+    def step():
+        y = solvers.apply(Lt, num, u)
+        gs.sweep(u.copy(), f)
+        return y
+    return n_unk, step, f"oracle (scipy CSR SpMV + colour-step GS) on {n_macros} macro(s) of the 480-macro shell at L={L}"
+
+
+def run_reference(a):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    L = min(a.L, 7)
+    n_unk, step, sample = oracle_sample(L, a.q, 1)
+    for _ in range(max(a.warmup, 0)):
+        step()
+    ts = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    value = 2 * n_unk / t / 1e9
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"shell t={a.t} n_r={a.nr} L={a.L} q={a.q} (sampled)",
+                      "sample": sample},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# GPU leg
+# ----------------------------------------------------------------------------
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import numpy as np
+    import torch
+
+    import paper_1608_06473_b200 as hhg
+    import synth
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    L, q = a.L, a.q
+    mesh = synth.shell_mesh(0.55, 1.0, a.t, a.nr)
+    t0 = time.time()
+    ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream)
+    ctx.fit(q, "lsqp", 2)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t0
+    n_local, n_owned, n_global = ctx.layout(L)
+    # inputs: seeded U[-1,1] on canonical ids (generated on the host once)
+    unk = np.ones(n_global, dtype=bool)
+    g = np.arange(n_global, dtype=np.int64)
+    u_g = synth.uniform_pm1(0, g)
+    f_g = synth.uniform_pm1(1, g)
+    del g, unk
+    u = ctx.zeros(L)
+    f = ctx.zeros(L)
+    y = ctx.zeros(L)
+    ctx.scatter_global(L, torch.from_numpy(u_g).to(dev), u)
+    ctx.scatter_global(L, torch.from_numpy(f_g).to(dev), f)
+    del u_g, f_g
+    torch.cuda.synchronize()
+
+    def step():
+        ctx.apply(L, u, y)
+        ctx.gs_sweep(L, u, f, 1)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = ctx.kernel_launches
+    ctx.profile(True)
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(a.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ctx.profile(False)
+    launches = ctx.kernel_launches - launches0
+    ms = ev0.elapsed_time(ev1) / a.steps
+    if dist:
+        tt = torch.tensor([ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    lups_step = 2 * n_owned * ws
+    value = lups_step / (ms * 1e-3) / 1e9
+    prof = ctx.profile_read()
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    # dominant kernel: volume kernels; algorithmic bytes per volume unknown:
+    # apply 16 B (u in, y out), GS 24 B (u in, f in, u out) -- SURVEY 8(d)
+    nvol = ctx.nt * ((2 ** L - 1) * (2 ** L - 2) * (2 ** L - 3) // 6)
+    va_ms, va_n = prof["vol_apply"]
+    vg_ms, vg_n = prof["vol_gs"]
+    roof = None
+    if va_n:
+        dom = max(("vol_apply", va_ms, 16), ("vol_gs", vg_ms, 24), key=lambda t: t[1])
+        name, tot_ms, bpu = dom
+        per_launch_bytes = nvol * bpu if name == "vol_apply" else nvol * 24 / 4
+        n_launch = va_n if name == "vol_apply" else vg_n
+        # GS: 4 colour launches per sweep together move 24 B per unknown
+        achieved = per_launch_bytes / (tot_ms / n_launch * 1e-3) / 1e9
+        roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "bytes_per_unknown": bpu, "share_of_step": tot_ms / (ms * a.steps)}
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"shell t={a.t} n_r={a.nr} ({mesh.nt} macros) L={L} q={q} LSQP j=2, "
+                                  f"apply + 1 GS sweep", "unknowns": n_owned * ws,
+                      "macros_per_gpu": mesh.nt, "parallelism": "replicas" if ws > 1 else "1 GPU",
+                      "l2": "inputs larger than L2 (1 vector = %.2f GB)" % (n_local * 8 / 1e9),
+                      "setup_s": round(t_setup, 2)},
+           "gpu_launches": launches,
+           "roofline": roof,
+           "clocks": clk.summary(),
+           "profile_ms": prof}
+    if rank == 0 and not a.no_extras:
+        out["e2e"] = e2e(ctx, L, u, f, y, a, n_owned, ws)
+        out["comparisons"] = comparisons(ctx, L, u, y, n_owned)
+    if rank == 0 and not a.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(L, q)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def e2e(ctx, L, u, f, y, a, n_owned, ws):
+    """Same metric through the C-ABI with HOST buffers: the library stages
+    u (apply), u and f (GS) host->device and y, u device->host every step."""
+    import torch
+    hu = u.cpu().pin_memory()
+    hf = f.cpu().pin_memory()
+    hy = torch.empty_like(hu).pin_memory()
+    step = lambda: (ctx.apply(L, hu.numpy(), hy.numpy()), ctx.gs_sweep(L, hu.numpy(), hf.numpy(), 1))
+    step()
+    torch.cuda.synchronize()
+    n = max(1, min(a.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        step()
+    torch.cuda.synchronize()
+    t = (time.perf_counter() - t0) / n
+    nb = hu.numel() * 8
+    return {"value": 2 * n_owned * ws / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": 3 * nb,
+            "d2h_bytes_per_step": 2 * nb, "ms_per_step": t * 1e3}
+
+
+def comparisons(ctx, L, u, y, n_owned):
+    """Comparison operators on the same workload (a11/a12): element-wise
+    on-the-fly FEM apply and constant-stencil (affine) apply, GLUP/s."""
+    import torch
+    res = {}
+    for op, reps in (("surrogate", 5), ("const", 5), ("fem", 2)):
+        ctx.apply(L, u, y, op=op)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            ctx.apply(L, u, y, op=op)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        res[f"{op}_apply"] = {"ms": ms, "glups": n_owned / (ms * 1e-3) / 1e9}
+    return res
+
+
+def cpu_baseline(L, q):
+    try:
+        n_unk, step, sample = oracle_sample(min(L, 7), q, 1)
+        step()
+        ts = []
+        t_end = time.time() + 15
+        while time.time() < t_end or len(ts) < 2:
+            t0 = time.perf_counter()
+            step()
+            ts.append(time.perf_counter() - t0)
+        t = statistics.median(ts)
+        return {"value": 2 * n_unk / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": sample + f", {len(ts)} reps, median"}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
+
+
+if __name__ == "__main__":
+    main()

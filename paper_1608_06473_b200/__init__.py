@@ -1,0 +1,196 @@
+"""Python binding of libhhg (include/hhg.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA library; this module only turns
+torch tensors / numpy arrays into pointers and status codes into exceptions.
+There is no CPU fallback: if libhhg.so is missing or fails to load, importing
+`lib()` raises.  Build with `python -c "import __graft_entry__ as g; g.build()"`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhhg.so")
+
+OPS = {"surrogate": 0, "fem": 1, "fem_elementwise": 1, "const": 2, "const_affine": 2}
+FIT = {"lsqp": 0, "ipoly": 1}
+STATUS = {0: "HHG_OK", 1: "HHG_ERR_INVALID", 2: "HHG_ERR_MESH", 3: "HHG_ERR_FIT",
+          4: "HHG_ERR_NUMERIC", 5: "HHG_ERR_DIVERGED", 6: "HHG_ERR_CUDA", 7: "HHG_ERR_NCCL",
+          8: "HHG_ERR_OOM", 9: "HHG_ERR_STATE"}
+
+_lib = None
+
+
+class HHGError(RuntimeError):
+    def __init__(self, status, msg=""):
+        self.status = status
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+
+
+def lib():
+    """Load libhhg.so (fails loudly; no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build()")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.hhg_setup_macro_mesh.argtypes = [P, P, I64, P, I64, P, I32, P, I32, I32, P, P, ctypes.POINTER(P)]
+    L.hhg_fit_surrogates.argtypes = [P, I32, I32, I32]
+    L.hhg_vector_layout.argtypes = [P, I32, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    L.hhg_apply.argtypes = [P, I32, I32, P, P]
+    L.hhg_residual.argtypes = [P, I32, I32, P, P, P, P]
+    L.hhg_gs_sweep.argtypes = [P, I32, I32, P, P, I32]
+    L.hhg_vcycle.argtypes = [P, I32, I32, I32, I32, I32, I32, P, P, I32, P]
+    L.hhg_gather_global.argtypes = [P, I32, P, P]
+    L.hhg_scatter_global.argtypes = [P, I32, P, P]
+    L.hhg_sync_copies.argtypes = [P, I32, P]
+    L.hhg_eval_stencils.argtypes = [P, I32, I32, I64, P]
+    L.hhg_kernel_launches.argtypes = [P]
+    L.hhg_kernel_launches.restype = I64
+    L.hhg_last_error.argtypes = [P]
+    L.hhg_last_error.restype = ctypes.c_char_p
+    L.hhg_destroy.argtypes = [P]
+    for name in ("hhg_setup_macro_mesh", "hhg_fit_surrogates", "hhg_vector_layout", "hhg_apply",
+                 "hhg_residual", "hhg_gs_sweep", "hhg_vcycle", "hhg_gather_global",
+                 "hhg_scatter_global", "hhg_sync_copies", "hhg_eval_stencils"):
+        getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _ptr(x, n=None, writable=False):
+    """Raw pointer of a float64 torch tensor (cuda or cpu) or numpy array."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("numpy vectors must be C-contiguous float64")
+        if n is not None and x.size < n:
+            raise ValueError(f"vector too short: {x.size} < {n}")
+        return x.ctypes.data
+    import torch
+    if not isinstance(x, torch.Tensor):
+        raise TypeError(type(x))
+    if x.dtype != torch.float64 or not x.is_contiguous():
+        raise ValueError("torch vectors must be contiguous float64")
+    if n is not None and x.numel() < n:
+        raise ValueError(f"vector too short: {x.numel()} < {n}")
+    return x.data_ptr()
+
+
+class Ctx:
+    """One hhg context (macro mesh + all levels 2..L_max) on the current device."""
+
+    def __init__(self, vertices, radius, tets, dirichlet, L_max, stream=None, owner=None,
+                 rank=0, nranks=1, nccl_id=None):
+        L = lib()
+        self._lib = L
+        v = np.ascontiguousarray(vertices, dtype=np.float64)
+        r = None if radius is None else np.ascontiguousarray(radius, dtype=np.float64)
+        t = np.ascontiguousarray(tets, dtype=np.int64)
+        d = np.ascontiguousarray(dirichlet, dtype=np.uint8)
+        o = None if owner is None else np.ascontiguousarray(owner, dtype=np.int32)
+        if stream is None:
+            try:
+                import torch
+                stream = torch.cuda.current_stream().cuda_stream if torch.cuda.is_available() else 0
+            except Exception:
+                stream = 0
+        h = ctypes.c_void_p()
+        st = L.hhg_setup_macro_mesh(v.ctypes.data, None if r is None else r.ctypes.data, v.shape[0],
+                                    t.ctypes.data, t.shape[0], d.ctypes.data, int(L_max),
+                                    None if o is None else o.ctypes.data, rank, nranks, nccl_id,
+                                    ctypes.c_void_p(stream), ctypes.byref(h))
+        if st != 0:
+            raise HHGError(st, "hhg_setup_macro_mesh failed (see stderr)")
+        self.h = h
+        self.L_max = int(L_max)
+        self.nt = t.shape[0]
+
+    @classmethod
+    def from_mesh(cls, mesh, L_max, **kw):
+        return cls(mesh.vertices, mesh.radius, mesh.tets, mesh.dirichlet, L_max, **kw)
+
+    def _check(self, st):
+        if st != 0:
+            raise HHGError(st, self._lib.hhg_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._lib.hhg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------------
+    def fit(self, q=2, method="lsqp", j=2):
+        self._check(self._lib.hhg_fit_surrogates(self.h, q, FIT[method], j))
+
+    def layout(self, L):
+        a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        self._check(self._lib.hhg_vector_layout(self.h, L, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c)))
+        return a.value, b.value, c.value
+
+    def zeros(self, L, device="cuda"):
+        import torch
+        return torch.zeros(self.layout(L)[0], dtype=torch.float64, device=device)
+
+    def apply(self, L, u, y, op="surrogate"):
+        n = self.layout(L)[0]
+        self._check(self._lib.hhg_apply(self.h, L, OPS[op], _ptr(u, n), _ptr(y, n)))
+        return y
+
+    def residual(self, L, u, f, r, op="surrogate", norm=False):
+        n = self.layout(L)[0]
+        nv = ctypes.c_double()
+        self._check(self._lib.hhg_residual(self.h, L, OPS[op], _ptr(u, n), _ptr(f, n), _ptr(r, n),
+                                           ctypes.byref(nv) if norm else None))
+        return nv.value if norm else None
+
+    def gs_sweep(self, L, u, f, n_sweeps=1, op="surrogate"):
+        n = self.layout(L)[0]
+        self._check(self._lib.hhg_gs_sweep(self.h, L, OPS[op], _ptr(u, n), _ptr(f, n), n_sweeps))
+        return u
+
+    def vcycle(self, L, u, f, n_cycles=1, nu1=3, nu2=3, L_coarse=2, cg_iters=50, op="surrogate"):
+        n = self.layout(L)[0]
+        hist = np.zeros(n_cycles + 1)
+        self._check(self._lib.hhg_vcycle(self.h, L, nu1, nu2, L_coarse, cg_iters, OPS[op], _ptr(u, n),
+                                         _ptr(f, n), n_cycles, hist.ctypes.data))
+        return hist
+
+    def gather_global(self, L, local, out=None):
+        n, _, ng = self.layout(L)
+        if out is None:
+            out = np.zeros(ng)
+        self._check(self._lib.hhg_gather_global(self.h, L, _ptr(local, n), _ptr(out, ng)))
+        return out
+
+    def scatter_global(self, L, glob, local):
+        n, _, ng = self.layout(L)
+        self._check(self._lib.hhg_scatter_global(self.h, L, _ptr(glob, ng), _ptr(local, n)))
+        return local
+
+    def sync_copies(self, L, local):
+        self._check(self._lib.hhg_sync_copies(self.h, L, _ptr(local, self.layout(L)[0])))
+        return local
+
+    def eval_stencils(self, L, macro=0, op="surrogate"):
+        N = 2 ** L
+        n_int = (N - 1) * (N - 2) * (N - 3) // 6
+        out = np.zeros((n_int, 15))
+        self._check(self._lib.hhg_eval_stencils(self.h, L, OPS[op], macro, out.ctypes.data))
+        return out
+
+    @property
+    def kernel_launches(self):
+        return int(self._lib.hhg_kernel_launches(self.h))

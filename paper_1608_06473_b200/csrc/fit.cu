@@ -1,0 +1,195 @@
+// Surrogate fit (setup) and the stencil test export.
+//
+// PAPER.md:501-534 (LSQP: a = argmin |A z - b|_2, sampling sets
+// S_l = M_m(l,j), m(l,j) = min{l, max{1,j}}), PAPER.md:471-499 (IPOLY, 10 P2
+// points of the shrunk tet), PAPER.md:647-668 (15 polynomials per macro and
+// level, computed once in a setup phase), PAPER.md:1236-1238 (DGESV/DGELS).
+// The sampling matrix A depends only on the level, so A^+ = R^-1 Q^T is formed
+// once per level on the host by Householder QR and applied to all macros and
+// all 15 right-hand sides as one batched product on the GPU.
+#include <cmath>
+
+#include "fem_device.cuh"
+#include "hhg_internal.h"
+
+namespace hhg {
+
+// Householder QR of A (n x m, row-major, n >= m) -> pinv (m x n) = R^-1 Q^T.
+static bool pinv_qr(std::vector<double> A, int64_t n, int m, std::vector<double>& pinv) {
+  std::vector<std::vector<double>> V(m);
+  std::vector<double> beta(m, 0.0);
+  std::vector<double> R(m * m, 0.0);
+  for (int j = 0; j < m; ++j) {
+    double norm = 0.0;
+    for (int64_t i = j; i < n; ++i) norm += A[i * m + j] * A[i * m + j];
+    norm = std::sqrt(norm);
+    double alpha = A[j * m + j] > 0 ? -norm : norm;
+    std::vector<double>& v = V[j];
+    v.assign(n - j, 0.0);
+    for (int64_t i = j; i < n; ++i) v[i - j] = A[i * m + j];
+    v[0] -= alpha;
+    double vv = 0.0;
+    for (double x : v) vv += x * x;
+    beta[j] = vv > 0 ? 2.0 / vv : 0.0;
+    for (int c = j; c < m; ++c) {
+      double s = 0.0;
+      for (int64_t i = j; i < n; ++i) s += v[i - j] * A[i * m + c];
+      s *= beta[j];
+      for (int64_t i = j; i < n; ++i) A[i * m + c] -= s * v[i - j];
+    }
+  }
+  double rmax = 0.0;
+  for (int j = 0; j < m; ++j) {
+    for (int c = j; c < m; ++c) R[j * m + c] = A[j * m + c];
+    rmax = std::max(rmax, std::fabs(R[j * m + j]));
+  }
+  for (int j = 0; j < m; ++j)
+    if (!(std::fabs(R[j * m + j]) > 1e-12 * rmax)) return false;
+  // Q_thin (n x m) = H_0 ... H_{m-1} [I; 0]
+  std::vector<double> Q(n * m, 0.0);
+  for (int j = 0; j < m; ++j) Q[j * m + j] = 1.0;
+  for (int j = m - 1; j >= 0; --j) {
+    const std::vector<double>& v = V[j];
+    for (int c = 0; c < m; ++c) {
+      double s = 0.0;
+      for (int64_t i = j; i < n; ++i) s += v[i - j] * Q[i * m + c];
+      s *= beta[j];
+      for (int64_t i = j; i < n; ++i) Q[i * m + c] -= s * v[i - j];
+    }
+  }
+  // pinv = R^-1 Q^T : solve R X = Q^T column by column (X m x n)
+  pinv.assign(m * n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int r = m - 1; r >= 0; --r) {
+      double s = Q[i * m + r];
+      for (int c = r + 1; c < m; ++c) s -= R[r * m + c] * pinv[c * n + i];
+      pinv[r * n + i] = s / R[r * m + r];
+    }
+  }
+  return true;
+}
+
+// B[T][s][w] = exact stencil at sample s of macro T
+__global__ void k_sample_stencils(const double* __restrict__ geo, int N, const int* __restrict__ smp,
+                                  int64_t ns, bool blended, double* __restrict__ B) {
+  int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t T = blockIdx.y;
+  if (s >= ns) return;
+  double w[15];
+  fem_partial(geo + T * 16, N, smp[3 * s], smp[3 * s + 1], smp[3 * s + 2], blended, w);
+  for (int q = 0; q < 15; ++q) B[(T * ns + s) * 15 + q] = w[q];
+}
+
+// coef[T][w][c] = (sum_s pinv[c][s] B[T][s][w]) * scale[c]
+__global__ void k_fit_coef(const double* __restrict__ pinv, const double* __restrict__ B, int64_t ns,
+                           int mq, const double* __restrict__ scale, double* __restrict__ coef) {
+  int64_t T = blockIdx.x;
+  int t = threadIdx.x;
+  if (t >= 15 * mq) return;
+  int w = t / mq, c = t % mq;
+  double acc = 0.0;
+  const double* b = B + T * ns * 15;
+  for (int64_t s = 0; s < ns; ++s) acc += pinv[c * ns + s] * b[s * 15 + w];
+  coef[(T * 15 + w) * mq + c] = acc * scale[c];
+}
+
+// Level 2 (l = 0): single interior node, exact stencil as the constant term.
+__global__ void k_exact_const(const double* __restrict__ geo, int N, int mq, bool blended,
+                              double* __restrict__ coef) {
+  int64_t T = blockIdx.x;
+  if (threadIdx.x != 0) return;
+  double w[15];
+  fem_partial(geo + T * 16, N, 1, 1, 1, blended, w);
+  for (int q = 0; q < 15; ++q) {
+    coef[(T * 15 + q) * mq] = w[q];
+    for (int c = 1; c < mq; ++c) coef[(T * 15 + q) * mq + c] = 0.0;
+  }
+}
+
+}  // namespace hhg
+
+using namespace hhg;
+
+extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method method, int sampling_j) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c) return HHG_ERR_INVALID;
+  if (c->poisoned) return HHG_ERR_CUDA;
+  if (q < 0 || q > 4) return set_err(c, HHG_ERR_INVALID, "q must be in 0..4 (PAPER.md:530-534)");
+  if (method != HHG_FIT_LSQP && method != HHG_FIT_IPOLY) return set_err(c, HHG_ERR_INVALID, "method");
+  if (method == HHG_FIT_IPOLY && q != 2)
+    return set_err(c, HHG_ERR_INVALID, "IPOLY points are defined for q = 2 (PAPER.md:490-499)");
+  const int mq = n_coeffs(q);
+  std::vector<int> el, em, en;
+  exponents(q, el, em, en);
+  for (int L = 2; L <= c->L_max; ++L) {
+    Level& lv = c->levels[L];
+    const int N = lv.N;
+    if (lv.d_coef) cudaFree(lv.d_coef);
+    lv.d_coef = nullptr;
+    HHG_CK(c, cudaMalloc(&lv.d_coef, c->nt_local * 15 * mq * sizeof(double)));
+    lv.q = q;
+    lv.mq = mq;
+    if (L == 2) {
+      k_exact_const<<<(unsigned)c->nt_local, 32, 0, c->stream>>>(c->d_geo, N, mq, c->blended, lv.d_coef);
+      HHG_LAUNCHED(c);
+      lv.fitted = true;
+      continue;
+    }
+    // sampling set
+    std::vector<int> smp;
+    if (method == HHG_FIT_IPOLY) {
+      int l = L - 2;
+      int a = (1 << (l + 2)) - 3, b = (1 << (l + 1)) - 1;
+      int pts[10][3] = {{1, 1, 1}, {1, 1, a}, {1, a, 1}, {a, 1, 1}, {1, 1, b},
+                        {1, b, 1}, {b, 1, 1}, {1, b, b}, {b, 1, b}, {b, b, 1}};
+      for (auto& p : pts) smp.insert(smp.end(), p, p + 3);
+    } else {
+      int l = L - 2;
+      int m = std::min(l, std::max(1, sampling_j));
+      int Nm = 1 << (m + 2), sc = 1 << (l - m);
+      for (int k = 1; k < Nm; ++k)
+        for (int j = 1; j < Nm - k; ++j)
+          for (int i = 1; i < Nm - k - j; ++i) {
+            smp.push_back(i * sc);
+            smp.push_back(j * sc);
+            smp.push_back(k * sc);
+          }
+    }
+    const int64_t ns = (int64_t)smp.size() / 3;
+    if (ns < mq) return set_err(c, HHG_ERR_FIT, "fewer sampling points than coefficients");
+    std::vector<double> A(ns * mq);
+    for (int64_t s = 0; s < ns; ++s)
+      for (int cc = 0; cc < mq; ++cc)
+        A[s * mq + cc] = std::pow((double)smp[3 * s] / N, el[cc]) *
+                         std::pow((double)smp[3 * s + 1] / N, em[cc]) *
+                         std::pow((double)smp[3 * s + 2] / N, en[cc]);
+    std::vector<double> pinv;
+    if (!pinv_qr(A, ns, mq, pinv))
+      return set_err(c, HHG_ERR_FIT, "rank-deficient sampling matrix at level " + std::to_string(L));
+    // index-unit scaling: x = i/N => a_lmn / N^(l+m+n) (exact powers of two)
+    std::vector<double> scale(mq);
+    for (int cc = 0; cc < mq; ++cc) scale[cc] = std::ldexp(1.0, -L * (el[cc] + em[cc] + en[cc]));
+    int* d_smp;
+    double *d_pinv, *d_B, *d_scale;
+    HHG_CK(c, cudaMalloc(&d_smp, smp.size() * sizeof(int)));
+    HHG_CK(c, cudaMalloc(&d_pinv, pinv.size() * sizeof(double)));
+    HHG_CK(c, cudaMalloc(&d_B, c->nt_local * ns * 15 * sizeof(double)));
+    HHG_CK(c, cudaMalloc(&d_scale, mq * sizeof(double)));
+    HHG_CK(c, cudaMemcpyAsync(d_smp, smp.data(), smp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    HHG_CK(c, cudaMemcpyAsync(d_pinv, pinv.data(), pinv.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    HHG_CK(c, cudaMemcpyAsync(d_scale, scale.data(), mq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    dim3 g1((unsigned)((ns + 127) / 128), (unsigned)c->nt_local);
+    k_sample_stencils<<<g1, 128, 0, c->stream>>>(c->d_geo, N, d_smp, ns, c->blended, d_B);
+    HHG_LAUNCHED(c);
+    k_fit_coef<<<(unsigned)c->nt_local, ((15 * mq + 31) / 32) * 32, 0, c->stream>>>(d_pinv, d_B, ns, mq, d_scale,
+                                                                               lv.d_coef);
+    HHG_LAUNCHED(c);
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(d_smp);
+    cudaFree(d_pinv);
+    cudaFree(d_B);
+    cudaFree(d_scale);
+    lv.fitted = true;
+  }
+  return HHG_OK;
+}

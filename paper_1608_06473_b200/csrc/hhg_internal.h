@@ -1,0 +1,185 @@
+// Internal declarations of libhhg (not part of the ABI; see include/hhg.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/hhg.h"
+
+namespace hhg {
+
+// ---------------------------------------------------------------------------
+// Stencil directions (reading R7); opposite(w) = 14 - w.
+// ---------------------------------------------------------------------------
+constexpr int kMC = 7;
+#define HHG_DIRS_INIT                                                                     \
+  {{0, 0, -1}, {1, 0, -1}, {0, 1, -1}, {-1, 1, -1}, {0, -1, 0}, {1, -1, 0}, {-1, 0, 0}, \
+   {0, 0, 0},  {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},   {1, -1, 1}, {0, -1, 1}, {-1, 0, 1}, \
+   {0, 0, 1}}
+extern const int kDirHost[15][3];
+
+// ---------------------------------------------------------------------------
+// Lattice layout helpers (host + device).  pos(i,j,k) = planeoff(k) + col(i,j)
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int64_t tri3(int64_t M) { return (M + 1) * (M + 2) * (M + 3) / 6; }
+__host__ __device__ inline int64_t plane_off(int N, int k) { return tri3(N) - tri3(N - k); }
+__host__ __device__ inline int64_t col_idx(int i, int j) {
+  int64_t d = i + j;
+  return d * (d + 1) / 2 + j;
+}
+__host__ __device__ inline int64_t lattice_pos(int N, int i, int j, int k) {
+  return plane_off(N, k) + col_idx(i, j);
+}
+__host__ __device__ inline int64_t n_lattice(int N) { return tri3(N); }
+__host__ __device__ inline int64_t n_interior(int N) {
+  return (int64_t)(N - 1) * (N - 2) * (N - 3) / 6;
+}
+// canonical volume index (k outer, j, i inner) of interior node (DESIGN.md numbering)
+__host__ __device__ inline int64_t vol_index(int N, int i, int j, int k) {
+  int64_t M = N - 1 - k;
+  auto c3 = [](int64_t n) { return n * (n - 1) * (n - 2) / 6; };
+  return (c3(N - 1) - c3(M + 1)) + (int64_t)(j - 1) * M - (int64_t)(j - 1) * j / 2 + (i - 1);
+}
+
+// Per-level geometry of the canonical numbering.
+struct GidInfo {
+  int N;
+  int64_t nv, n_e, n_f;
+  int64_t nfi, nvi;
+  int64_t base_e, base_f, base_v, n_total;
+};
+
+// Topology tables of one macro (global ids) -- host and device copies.
+struct MacroTopo {
+  int64_t gv[4];   // global vertex ids of local vertices
+  int64_t e[6];    // edge ids of local pairs (0,1),(0,2),(0,3),(1,2),(1,3),(2,3)
+  int64_t f[4];    // face ids of faces opposite local vertex 0..3
+  int64_t gT;      // global macro index
+};
+
+__host__ __device__ inline int local_edge(int a, int b) {
+  if (a > b) { int t = a; a = b; b = t; }
+  // (0,1)0 (0,2)1 (0,3)2 (1,2)3 (1,3)4 (2,3)5
+  return a == 0 ? b - 1 : (a == 1 ? b + 1 : 5);
+}
+
+// Canonical global id of lattice node (i,j,k) of a macro (DESIGN.md numbering).
+__host__ __device__ inline int64_t node_gid(const GidInfo& g, const MacroTopo& t, int i, int j,
+                                            int k) {
+  const int N = g.N;
+  int w[4] = {N - i - j - k, i, j, k};
+  int sup[4];
+  int ns = 0;
+  for (int v = 0; v < 4; ++v)
+    if (w[v] > 0) sup[ns++] = v;
+  if (ns == 1) return t.gv[sup[0]];
+  if (ns == 2) {
+    int p = sup[0], q = sup[1];
+    int64_t e = t.e[local_edge(p, q)];
+    int m = (t.gv[p] > t.gv[q]) ? w[p] : w[q];  // weight of the larger-id endpoint
+    return g.base_e + e * (N - 1) + (m - 1);
+  }
+  if (ns == 3) {
+    int lf = 0;
+    for (int v = 0; v < 4; ++v)
+      if (w[v] == 0) lf = v;
+    // sort the 3 support vertices by global id
+    int a = sup[0], b = sup[1], c = sup[2];
+    if (t.gv[a] > t.gv[b]) { int x = a; a = b; b = x; }
+    if (t.gv[b] > t.gv[c]) { int x = b; b = c; c = x; }
+    if (t.gv[a] > t.gv[b]) { int x = a; a = b; b = x; }
+    int64_t s = w[b], tt = w[c];
+    int64_t idx = (tt - 1) * (N - 1) - (tt - 1) * tt / 2 + (s - 1);
+    return g.base_f + t.f[lf] * g.nfi + idx;
+  }
+  return g.base_v + t.gT * g.nvi + vol_index(N, i, j, k);
+}
+
+// ---------------------------------------------------------------------------
+// Per-level state
+// ---------------------------------------------------------------------------
+enum { kStepVertex = 0, kStepEdge0, kStepEdge1, kStepFace0, kStepFace1, kStepFace2, kNumLpSteps };
+
+struct Level {
+  int L = 0, N = 0;
+  int64_t P = 0;        // lattice nodes per macro
+  int64_t S = 0;        // stride (doubles) per macro
+  int64_t n_local = 0;  // doubles per local vector
+  int64_t n_owned = 0;  // owned unknowns
+  GidInfo gi{};
+  // lower-primitive rows (owned unknowns on vertices/edges/faces)
+  int64_t n_rows = 0, nnz = 0, n_copies = 0, n_dir = 0;
+  int64_t step_start[kNumLpSteps + 1] = {0};
+  uint64_t* d_row_ptr = nullptr;   // [n_rows+1]
+  uint32_t* d_col = nullptr;       // [nnz] local slot; entry 0 of a row = centre
+  double* d_val = nullptr;         // [nnz] exact FEM, blended
+  double* d_val_cons = nullptr;    // [nnz] exact FEM, affine
+  uint64_t* d_copy_ptr = nullptr;  // [n_rows+1]
+  uint32_t* d_copy = nullptr;      // [n_copies] slots, ascending (first = owner)
+  int64_t* d_row_gid = nullptr;    // [n_rows]
+  uint32_t* d_dir_slot = nullptr;  // [n_dir] Dirichlet slots (all copies)
+  int64_t* d_dir_gid = nullptr;    // [n_dir]
+  double* d_tmp = nullptr;         // [n_rows] GS scratch
+  // volume coefficients
+  int q = -1;
+  int mq = 0;
+  double* d_coef = nullptr;        // [nt_local][15][mq] index units, exponent order kExp
+  double* d_cons = nullptr;        // [nt_local][15] affine constant stencil
+  bool fitted = false;
+};
+
+struct Ctx {
+  std::string err;
+  bool poisoned = false;
+  cudaStream_t stream = nullptr;
+  int rank = 0, nranks = 1;
+  int L_max = 0;
+  int64_t nv = 0, nt = 0, nt_local = 0;
+  int64_t n_e = 0, n_f = 0;
+  bool blended = true;
+  std::vector<double> vertices, radius;
+  std::vector<int64_t> tets;
+  std::vector<uint8_t> dirichlet;
+  std::vector<int64_t> local_macros;  // global ids of local macros
+  std::vector<MacroTopo> topo;        // [nt_local]
+  MacroTopo* d_topo = nullptr;
+  double* d_geo = nullptr;            // [nt_local][4][4]: x,y,z,r per local vertex
+  std::vector<Level> levels;          // index L
+  int64_t launches = 0;
+  // host-vector staging
+  double* d_stage[4] = {nullptr, nullptr, nullptr, nullptr};
+  int64_t stage_n = 0;
+  double* d_red = nullptr;            // reduction scratch
+  double* h_red = nullptr;            // pinned
+  int64_t red_n = 0;
+};
+
+// error helpers ------------------------------------------------------------
+hhg_status set_err(Ctx* c, hhg_status s, const std::string& msg);
+hhg_status check_cuda(Ctx* c, cudaError_t e, const char* what);
+#define HHG_CK(c, call)                                        \
+  do {                                                         \
+    cudaError_t e__ = (call);                                  \
+    if (e__ != cudaSuccess) return hhg::check_cuda(c, e__, #call); \
+  } while (0)
+#define HHG_LAUNCHED(c)                                                    \
+  do {                                                                     \
+    (c)->launches++;                                                       \
+    cudaError_t e__ = cudaGetLastError();                                  \
+    if (e__ != cudaSuccess) return hhg::check_cuda(c, e__, "kernel launch"); \
+  } while (0)
+
+// exponent table for the surrogate basis (index units): for q, m_q entries
+int n_coeffs(int q);
+void exponents(int q, std::vector<int>& l, std::vector<int>& m, std::vector<int>& n);
+
+// Device geometry helpers (fem.cu)
+hhg_status launch_fem_partial(Ctx* c, int L, const uint32_t* d_slots, int64_t n, bool blended,
+                              double* d_out15);
+hhg_status build_lp_values(Ctx* c, Level& lv, const std::vector<uint8_t>& cmap);
+
+}  // namespace hhg

@@ -1,0 +1,424 @@
+// Operator entry points: apply, residual, multicolour GS, gather/scatter,
+// stencil export.  Baseline ("v1") volume kernels: one thread per lattice node.
+//
+// PAPER.md:618-636 (L~: volume rows from the surrogate, lower primitives from
+// exact FEM), PAPER.md:654-657 (15 polynomials evaluated per node),
+// PAPER.md:862-871 (residual), PAPER.md:1306-1315 (eq. iteration-scheme:
+// u_I = (f_I - sum_{w != mc} s_w u_{I_w}) / s_mc).
+#include <cstring>
+
+#include "fem_device.cuh"
+#include "hhg_internal.h"
+#include "vol_kernels.cuh"
+
+namespace hhg {
+
+// ---------------------------------------------------------------------------
+// Lower-primitive rows (stored exact FEM rows, CSR; entry 0 = centre)
+// ---------------------------------------------------------------------------
+__global__ void k_lp_apply(int64_t r0, int64_t r1, const uint64_t* __restrict__ rp,
+                           const uint32_t* __restrict__ col, const double* __restrict__ val,
+                           const uint64_t* __restrict__ cp, const uint32_t* __restrict__ copy,
+                           const double* __restrict__ u, const double* __restrict__ f,
+                           double* __restrict__ out, int mode) {
+  int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  double acc = 0.0;
+  const uint64_t e0 = rp[r], e1 = rp[r + 1];
+  for (uint64_t e = e0; e < e1; ++e) acc += val[e] * u[col[e]];
+  double res = mode == kModeResid ? f[col[e0]] - acc : acc;
+  for (uint64_t c = cp[r]; c < cp[r + 1]; ++c) out[copy[c]] = res;
+}
+
+__global__ void k_lp_gs_compute(int64_t r0, int64_t r1, const uint64_t* __restrict__ rp,
+                                const uint32_t* __restrict__ col, const double* __restrict__ val,
+                                const double* __restrict__ u, const double* __restrict__ f,
+                                double* __restrict__ tmp) {
+  int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  const uint64_t e0 = rp[r], e1 = rp[r + 1];
+  double acc = f[col[e0]];
+  for (uint64_t e = e0 + 1; e < e1; ++e) acc -= val[e] * u[col[e]];
+  tmp[r] = acc / val[e0];
+}
+
+__global__ void k_lp_write(int64_t r0, int64_t r1, const uint64_t* __restrict__ cp,
+                           const uint32_t* __restrict__ copy, const double* __restrict__ tmp,
+                           double* __restrict__ u) {
+  int64_t r = r0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  double v = tmp[r];
+  for (uint64_t c = cp[r]; c < cp[r + 1]; ++c) u[copy[c]] = v;
+}
+
+__global__ void k_lp_sync(int64_t n_rows, const uint64_t* __restrict__ cp,
+                          const uint32_t* __restrict__ copy, double* __restrict__ u) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  uint64_t c0 = cp[r];
+  double v = u[copy[c0]];
+  for (uint64_t c = c0 + 1; c < cp[r + 1]; ++c) u[copy[c]] = v;
+}
+
+__global__ void k_zero_slots(int64_t n, const uint32_t* __restrict__ slots, double* __restrict__ out) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < n) out[slots[t]] = 0.0;
+}
+
+// gather / scatter ------------------------------------------------------------
+__global__ void k_vol_gather(int N, int64_t S, int64_t P, const MacroTopo* __restrict__ topo,
+                             GidInfo gi, const double* __restrict__ local, double* __restrict__ glob,
+                             int dir) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t T = blockIdx.y;
+  if (p >= P) return;
+  int i, j, k;
+  decode_pos(N, p, i, j, k);
+  if (i < 1 || j < 1 || k < 1 || i + j + k > N - 1) return;
+  int64_t g = gi.base_v + topo[T].gT * gi.nvi + vol_index(N, i, j, k);
+  if (dir == 0) glob[g] = local[T * S + p];
+  else ((double*)local)[T * S + p] = glob[g];
+}
+
+__global__ void k_lp_gather(int64_t n_rows, const uint64_t* __restrict__ cp,
+                            const uint32_t* __restrict__ copy, const int64_t* __restrict__ gid,
+                            const double* __restrict__ local, double* __restrict__ glob, int dir) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  if (dir == 0) {
+    glob[gid[r]] = local[copy[cp[r]]];
+  } else {
+    double v = glob[gid[r]];
+    for (uint64_t c = cp[r]; c < cp[r + 1]; ++c) ((double*)local)[copy[c]] = v;
+  }
+}
+
+// sum of squares over unique unknowns (fixed grid => deterministic) ----------
+constexpr int kRedBlocks = 1184;
+__device__ inline double block_sum(double v) {
+  __shared__ double sh[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  }
+  return v;
+}
+
+__global__ void k_sumsq(int N, int64_t S, int64_t P, int64_t ntl, const double* __restrict__ r,
+                        int64_t n_rows, const uint32_t* __restrict__ lp_owner_col,
+                        const uint64_t* __restrict__ rp, double* __restrict__ part) {
+  double acc = 0.0;
+  const int64_t tot = ntl * P;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t T = t / P, p = t - T * P;
+    int i, j, k;
+    decode_pos(N, p, i, j, k);
+    if (i < 1 || j < 1 || k < 1 || i + j + k > N - 1) continue;
+    double v = r[T * S + p];
+    acc += v * v;
+  }
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_rows;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double v = r[lp_owner_col[rp[q]]];
+    acc += v * v;
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+__global__ void k_final_sum(const double* __restrict__ part, int n, double* __restrict__ out) {
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) acc += part[t];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) out[0] = acc;
+}
+
+// eval stencils export ---------------------------------------------------------
+__global__ void k_eval_stencils(int N, int64_t P, const double* __restrict__ geo,
+                                const double* __restrict__ coef, int mq, const double* __restrict__ cons,
+                                int op, bool blended, double* __restrict__ out) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int i, j, k;
+  decode_pos(N, p, i, j, k);
+  if (i < 1 || j < 1 || k < 1 || i + j + k > N - 1) return;
+  double s[15];
+  node_weights(op, N, i, j, k, geo, coef, mq, cons, blended, s);
+  int64_t idx = vol_index(N, i, j, k);
+  for (int w = 0; w < 15; ++w) out[idx * 15 + w] = s[w];
+}
+
+// ---------------------------------------------------------------------------
+// host helpers
+// ---------------------------------------------------------------------------
+static bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct Staged {
+  double* dev = nullptr;
+  const void* host = nullptr;
+  bool staged = false;
+};
+
+static hhg_status stage(Ctx* c, int slot, const void* p, int64_t n, bool copy_in, Staged& s) {
+  s.host = p;
+  if (is_device_ptr(p)) {
+    s.dev = (double*)p;
+    s.staged = false;
+    return HHG_OK;
+  }
+  if (c->stage_n < n) {
+    for (auto*& b : c->d_stage)
+      if (b) { cudaFree(b); b = nullptr; }
+    c->stage_n = n;
+  }
+  if (!c->d_stage[slot]) HHG_CK(c, cudaMalloc(&c->d_stage[slot], c->stage_n * sizeof(double)));
+  s.dev = c->d_stage[slot];
+  s.staged = true;
+  if (copy_in)
+    HHG_CK(c, cudaMemcpyAsync(s.dev, p, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  return HHG_OK;
+}
+
+static hhg_status unstage(Ctx* c, Staged& s, int64_t n) {
+  if (!s.staged) return HHG_OK;
+  HHG_CK(c, cudaMemcpyAsync((void*)s.host, s.dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  return HHG_OK;
+}
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
+  if (!c) return HHG_ERR_INVALID;
+  if (c->poisoned) return HHG_ERR_CUDA;
+  if (L < 2 || L > c->L_max) return set_err(c, HHG_ERR_INVALID, "L out of range");
+  if (op < 0 || op > 2) return set_err(c, HHG_ERR_INVALID, "bad op");
+  if (op == HHG_OP_SURROGATE && !c->levels[L].fitted)
+    return set_err(c, HHG_ERR_STATE, "hhg_fit_surrogates must be called before using the surrogate operator");
+  (void)smoother;
+  return HHG_OK;
+}
+
+// The volume pass of one operation (apply / residual / GS colour).
+static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
+                              const double* f, double* out) {
+  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
+  k_vol_v1<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_geo, lv.d_coef, lv.mq, lv.d_cons, op,
+                                        c->blended, mode, colour, u, f, out);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+static hhg_status lp_pass(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f,
+                          double* out) {
+  if (lv.n_rows == 0) return HHG_OK;
+  const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_val_cons : lv.d_val;
+  k_lp_apply<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(0, lv.n_rows, lv.d_row_ptr, lv.d_col, val,
+                                                         lv.d_copy_ptr, lv.d_copy, u, f, out, mode);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+static hhg_status zero_dir(Ctx* c, Level& lv, double* out) {
+  if (lv.n_dir == 0) return HHG_OK;
+  k_zero_slots<<<nblk(lv.n_dir, 256), 256, 0, c->stream>>>(lv.n_dir, lv.d_dir_slot, out);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out) {
+  if (c->red_n < kRedBlocks + 1) {
+    HHG_CK(c, cudaMalloc(&c->d_red, (kRedBlocks + 1) * sizeof(double)));
+    HHG_CK(c, cudaMallocHost(&c->h_red, 2 * sizeof(double)));
+    c->red_n = kRedBlocks + 1;
+  }
+  k_sumsq<<<kRedBlocks, 256, 0, c->stream>>>(lv.N, lv.S, lv.P, c->nt_local, r, lv.n_rows, lv.d_col,
+                                             lv.d_row_ptr, c->d_red);
+  HHG_LAUNCHED(c);
+  k_final_sum<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_red + kRedBlocks);
+  HHG_LAUNCHED(c);
+  HHG_CK(c, cudaMemcpyAsync(c->h_red, c->d_red + kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  *out = std::sqrt(c->h_red[0]);
+  return HHG_OK;
+}
+
+hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
+  const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_val_cons : lv.d_val;
+  for (int s = 0; s < kNumLpSteps; ++s) {
+    int64_t r0 = lv.step_start[s], r1 = lv.step_start[s + 1];
+    if (r1 <= r0) continue;
+    k_lp_gs_compute<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_row_ptr, lv.d_col, val, u, f,
+                                                               lv.d_tmp);
+    HHG_LAUNCHED(c);
+    k_lp_write<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_copy_ptr, lv.d_copy, lv.d_tmp, u);
+    HHG_LAUNCHED(c);
+  }
+  for (int col = 0; col < 4; ++col) {
+    hhg_status st = volume_pass(c, lv, op, kModeGS, col, u, f, u);
+    if (st != HHG_OK) return st;
+  }
+  return HHG_OK;
+}
+
+hhg_status apply_dev(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* y) {
+  hhg_status st;
+  if ((st = volume_pass(c, lv, op, mode, 0, u, f, y)) != HHG_OK) return st;
+  if ((st = lp_pass(c, lv, op, mode, u, f, y)) != HHG_OK) return st;
+  return zero_dir(c, lv, y);
+}
+
+}  // namespace hhg
+
+using namespace hhg;
+
+extern "C" hhg_status hhg_apply(hhg_ctx ctx, int L, hhg_op op, const double* u, double* y) {
+  Ctx* c = (Ctx*)ctx;
+  hhg_status st = check_call(c, L, op, false);
+  if (st != HHG_OK) return st;
+  if (!u || !y || u == y) return set_err(c, HHG_ERR_INVALID, "u, y must be non-NULL and distinct");
+  Level& lv = c->levels[L];
+  Staged su, sy;
+  if ((st = stage(c, 0, u, lv.n_local, true, su)) != HHG_OK) return st;
+  if ((st = stage(c, 1, y, lv.n_local, false, sy)) != HHG_OK) return st;
+  if ((st = apply_dev(c, lv, op, kModeApply, su.dev, nullptr, sy.dev)) != HHG_OK) return st;
+  return unstage(c, sy, lv.n_local);
+}
+
+extern "C" hhg_status hhg_residual(hhg_ctx ctx, int L, hhg_op op, const double* u, const double* f,
+                                   double* r, double* norm2) {
+  Ctx* c = (Ctx*)ctx;
+  hhg_status st = check_call(c, L, op, false);
+  if (st != HHG_OK) return st;
+  if (!u || !f || !r || r == u || r == f) return set_err(c, HHG_ERR_INVALID, "bad vectors");
+  Level& lv = c->levels[L];
+  Staged su, sf, sr;
+  if ((st = stage(c, 0, u, lv.n_local, true, su)) != HHG_OK) return st;
+  if ((st = stage(c, 1, f, lv.n_local, true, sf)) != HHG_OK) return st;
+  if ((st = stage(c, 2, r, lv.n_local, false, sr)) != HHG_OK) return st;
+  if ((st = apply_dev(c, lv, op, kModeResid, su.dev, sf.dev, sr.dev)) != HHG_OK) return st;
+  if (norm2 && (st = norm2_of(c, lv, sr.dev, norm2)) != HHG_OK) return st;
+  return unstage(c, sr, lv.n_local);
+}
+
+extern "C" hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n) {
+  Ctx* c = (Ctx*)ctx;
+  hhg_status st = check_call(c, L, op, true);
+  if (st != HHG_OK) return st;
+  if (!u || !f || (const double*)u == f || n < 0) return set_err(c, HHG_ERR_INVALID, "bad vectors");
+  Level& lv = c->levels[L];
+  Staged su, sf;
+  if ((st = stage(c, 0, u, lv.n_local, true, su)) != HHG_OK) return st;
+  if ((st = stage(c, 1, f, lv.n_local, true, sf)) != HHG_OK) return st;
+  for (int s = 0; s < n; ++s)
+    if ((st = gs_sweep_dev(c, lv, op, su.dev, sf.dev)) != HHG_OK) return st;
+  return unstage(c, su, lv.n_local);
+}
+
+extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local, double* glob) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || L < 2 || L > c->L_max || !local || !glob) return HHG_ERR_INVALID;
+  if (c->nranks != 1) return set_err(c, HHG_ERR_INVALID, "gather_global: single-rank only");
+  Level& lv = c->levels[L];
+  hhg_status st;
+  Staged sl;
+  if ((st = stage(c, 0, local, lv.n_local, true, sl)) != HHG_OK) return st;
+  // global may be larger than n_local: use a dedicated allocation if host
+  double* dglob = glob;
+  bool host_glob = !is_device_ptr(glob);
+  if (host_glob) HHG_CK(c, cudaMalloc(&dglob, lv.gi.n_total * sizeof(double)));
+  HHG_CK(c, cudaMemsetAsync(dglob, 0, lv.gi.n_total * sizeof(double), c->stream));
+  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
+  k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, sl.dev, dglob, 0);
+  HHG_LAUNCHED(c);
+  if (lv.n_rows) {
+    k_lp_gather<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy,
+                                                            lv.d_row_gid, sl.dev, dglob, 0);
+    HHG_LAUNCHED(c);
+  }
+  if (host_glob) {
+    HHG_CK(c, cudaMemcpyAsync(glob, dglob, lv.gi.n_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(dglob);
+  }
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob, double* local) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || L < 2 || L > c->L_max || !local || !glob) return HHG_ERR_INVALID;
+  if (c->nranks != 1) return set_err(c, HHG_ERR_INVALID, "scatter_global: single-rank only");
+  Level& lv = c->levels[L];
+  hhg_status st;
+  Staged sl;
+  if ((st = stage(c, 0, local, lv.n_local, false, sl)) != HHG_OK) return st;
+  const double* dglob = glob;
+  double* tmp = nullptr;
+  if (!is_device_ptr(glob)) {
+    HHG_CK(c, cudaMalloc(&tmp, lv.gi.n_total * sizeof(double)));
+    HHG_CK(c, cudaMemcpyAsync(tmp, glob, lv.gi.n_total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    dglob = tmp;
+  }
+  HHG_CK(c, cudaMemsetAsync(sl.dev, 0, lv.n_local * sizeof(double), c->stream));
+  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
+  k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, sl.dev, (double*)dglob, 1);
+  HHG_LAUNCHED(c);
+  if (lv.n_rows) {
+    k_lp_gather<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy,
+                                                            lv.d_row_gid, sl.dev, (double*)dglob, 1);
+    HHG_LAUNCHED(c);
+  }
+  if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
+  if ((st = unstage(c, sl, lv.n_local)) != HHG_OK) return st;
+  if (tmp) {
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(tmp);
+  }
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_sync_copies(hhg_ctx ctx, int L, double* local) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || L < 2 || L > c->L_max || !local) return HHG_ERR_INVALID;
+  Level& lv = c->levels[L];
+  hhg_status st;
+  Staged sl;
+  if ((st = stage(c, 0, local, lv.n_local, true, sl)) != HHG_OK) return st;
+  if (lv.n_rows) {
+    k_lp_sync<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy, sl.dev);
+    HHG_LAUNCHED(c);
+  }
+  if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
+  return unstage(c, sl, lv.n_local);
+}
+
+extern "C" hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t macro, double* out) {
+  Ctx* c = (Ctx*)ctx;
+  hhg_status st = check_call(c, L, op, false);
+  if (st != HHG_OK) return st;
+  if (macro < 0 || macro >= c->nt_local || !out) return set_err(c, HHG_ERR_INVALID, "bad macro/out");
+  Level& lv = c->levels[L];
+  int64_t n = n_interior(lv.N) * 15;
+  Staged so;
+  if ((st = stage(c, 3, out, std::max<int64_t>(n, lv.n_local), false, so)) != HHG_OK) return st;
+  const double* coef = lv.d_coef ? lv.d_coef + macro * 15 * lv.mq : nullptr;
+  k_eval_stencils<<<nblk(lv.P, 128), 128, 0, c->stream>>>(lv.N, lv.P, c->d_geo + macro * 16, coef, lv.mq,
+                                                         lv.d_cons + macro * 15, op, c->blended, so.dev);
+  HHG_LAUNCHED(c);
+  if (so.staged) {
+    HHG_CK(c, cudaMemcpyAsync(out, so.dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+  }
+  return HHG_OK;
+}

@@ -1,0 +1,511 @@
+// Host setup: mesh ingest/validation, topology, canonical numbering, per-level
+// layouts, lower-primitive rows, gather/scatter, errors (include/hhg.h).
+//
+// PAPER.md:202-207 (unstructured macro mesh T_-2), 295-338 (HHG primitives:
+// vertex/edge/face/volume; ghost copies of lower primitives), 321-327 (lower
+// primitive stencils assembled from local stiffness matrices), 372-379
+// (index set).  Canonical numbering: DESIGN.md.
+#include <omp.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "fem_device.cuh"
+#include "hhg_internal.h"
+
+namespace hhg {
+
+const int kDirHost[15][3] = HHG_DIRS_INIT;
+
+hhg_status set_err(Ctx* c, hhg_status s, const std::string& msg) {
+  if (c) c->err = msg;
+  return s;
+}
+
+hhg_status check_cuda(Ctx* c, cudaError_t e, const char* what) {
+  std::string m = std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e);
+  if (c) {
+    c->err = m;
+    c->poisoned = true;
+  }
+  if (e == cudaErrorMemoryAllocation) return HHG_ERR_OOM;
+  return HHG_ERR_CUDA;
+}
+
+int n_coeffs(int q) { return (q + 3) * (q + 2) * (q + 1) / 6; }
+
+void exponents(int q, std::vector<int>& l, std::vector<int>& m, std::vector<int>& n) {
+  l.clear(); m.clear(); n.clear();
+  for (int d = 0; d <= q; ++d)
+    for (int a = d; a >= 0; --a)
+      for (int b = d - a; b >= 0; --b) {
+        l.push_back(a); m.push_back(b); n.push_back(d - a - b);
+      }
+}
+
+namespace {
+
+struct RowDesc {
+  int8_t type;  // 0 vertex 1 edge 2 face
+  int32_t a, b; // edge: m ; face: s, t
+  int64_t id;   // vertex / edge / face id
+};
+
+struct Topology {
+  std::vector<int64_t> ekey, fkey;               // sorted unique keys
+  std::vector<std::vector<int32_t>> vinc, einc, finc;  // incident local macros
+  std::vector<uint8_t> vdir, edir, fdir;
+};
+
+inline void corner(int lv, int N, int w[4]) {
+  w[0] = w[1] = w[2] = w[3] = 0;
+  w[lv] = N;
+}
+
+}  // namespace
+
+static int local_of(const int64_t* tv, int64_t g) {
+  for (int v = 0; v < 4; ++v)
+    if (tv[v] == g) return v;
+  return -1;
+}
+
+// Build lower-primitive rows of one level.
+static hhg_status build_level(Ctx* c, Topology& tp, int L) {
+  Level& lv = c->levels[L];
+  const int N = 1 << L;
+  lv.L = L;
+  lv.N = N;
+  lv.P = n_lattice(N);
+  lv.S = (lv.P + 31) / 32 * 32;
+  lv.n_local = lv.S * c->nt_local;
+  GidInfo& g = lv.gi;
+  g.N = N;
+  g.nv = c->nv;
+  g.n_e = c->n_e;
+  g.n_f = c->n_f;
+  g.nfi = (int64_t)(N - 1) * (N - 2) / 2;
+  g.nvi = n_interior(N);
+  g.base_e = c->nv;
+  g.base_f = g.base_e + c->n_e * (N - 1);
+  g.base_v = g.base_f + c->n_f * g.nfi;
+  g.n_total = g.base_v + c->nt * g.nvi;
+
+  // ---- enumerate rows (owned unknown lower-primitive nodes) in GS step order
+  std::vector<RowDesc> rows;
+  std::vector<RowDesc> drows;  // Dirichlet lower nodes (all copies zeroed)
+  int64_t steps[kNumLpSteps + 1];
+  steps[0] = 0;
+  for (int64_t v = 0; v < c->nv; ++v) {
+    if (tp.vinc[v].empty()) continue;
+    (tp.vdir[v] ? drows : rows).push_back(RowDesc{0, 0, 0, v});
+  }
+  steps[1] = (int64_t)rows.size();
+  for (int col = 0; col < 2; ++col) {
+    for (int64_t e = 0; e < c->n_e; ++e)
+      for (int m = 1; m <= N - 1; ++m) {
+        if ((m % 2) != col) continue;
+        (tp.edir[e] ? drows : rows).push_back(RowDesc{1, m, 0, e});
+      }
+    steps[2 + col] = (int64_t)rows.size();
+  }
+  for (int col = 0; col < 3; ++col) {
+    for (int64_t f = 0; f < c->n_f; ++f)
+      for (int t = 1; t <= N - 2; ++t)
+        for (int s = 1; s <= N - 1 - t; ++s) {
+          if ((s + 2 * t) % 3 != col) continue;
+          (tp.fdir[f] ? drows : rows).push_back(RowDesc{2, s, t, f});
+        }
+    steps[4 + col] = (int64_t)rows.size();
+  }
+  for (int s = 0; s <= kNumLpSteps; ++s) lv.step_start[s] = steps[s];
+  lv.n_rows = (int64_t)rows.size();
+  lv.n_owned = lv.n_rows + c->nt_local * g.nvi;
+
+  const int64_t S = lv.S;
+  auto is_dir = [&](int64_t gid) -> bool {
+    if (gid < g.base_e) return tp.vdir[gid] != 0;
+    if (gid < g.base_f) return tp.edir[(gid - g.base_e) / (N - 1)] != 0;
+    if (gid < g.base_v) return tp.fdir[(gid - g.base_f) / g.nfi] != 0;
+    return false;
+  };
+  // copies of a row: (local macro, ijk)
+  auto copies_of = [&](const RowDesc& r, std::vector<std::array<int, 4>>& out) {
+    out.clear();
+    if (r.type == 0) {
+      for (int32_t T : tp.vinc[r.id]) {
+        int lvx = local_of(c->topo[T].gv, r.id);
+        int w[4];
+        corner(lvx, N, w);
+        out.push_back(std::array<int, 4>{{(int)T, w[1], w[2], w[3]}});
+      }
+    } else if (r.type == 1) {
+      int64_t a = tp.ekey[r.id] / c->nv, b = tp.ekey[r.id] % c->nv;
+      for (int32_t T : tp.einc[r.id]) {
+        int la = local_of(c->topo[T].gv, a), lb = local_of(c->topo[T].gv, b);
+        int w[4] = {0, 0, 0, 0};
+        w[la] = N - r.a;
+        w[lb] = r.a;
+        out.push_back(std::array<int, 4>{{(int)T, w[1], w[2], w[3]}});
+      }
+    } else {
+      int64_t key = tp.fkey[r.id];
+      int64_t cc = key % c->nv, ab = key / c->nv;
+      int64_t a = ab / c->nv, b = ab % c->nv;
+      for (int32_t T : tp.finc[r.id]) {
+        int la = local_of(c->topo[T].gv, a), lb = local_of(c->topo[T].gv, b),
+            lc = local_of(c->topo[T].gv, cc);
+        int w[4] = {0, 0, 0, 0};
+        w[la] = N - r.a - r.b;
+        w[lb] = r.a;
+        w[lc] = r.b;
+        out.push_back(std::array<int, 4>{{(int)T, w[1], w[2], w[3]}});
+      }
+    }
+    std::sort(out.begin(), out.end());
+  };
+  auto slot_of = [&](int T, int i, int j, int k) -> int64_t { return T * S + lattice_pos(N, i, j, k); };
+  auto row_gid = [&](const RowDesc& r) -> int64_t {
+    if (r.type == 0) return r.id;
+    if (r.type == 1) return g.base_e + r.id * (N - 1) + (r.a - 1);
+    int64_t s = r.a, t = r.b;
+    return g.base_f + r.id * g.nfi + (t - 1) * (N - 1) - (t - 1) * t / 2 + (s - 1);
+  };
+  if ((uint64_t)lv.n_local >= (1ull << 32))
+    return set_err(c, HHG_ERR_INVALID, "local vector exceeds 2^32 doubles at level " + std::to_string(L));
+
+  // ---- pass 1: counts
+  const int64_t nr = lv.n_rows;
+  std::vector<uint64_t> rp(nr + 1, 0), cp(nr + 1, 0);
+#pragma omp parallel
+  {
+    std::vector<std::array<int, 4>> cps;
+    std::vector<int64_t> cols;
+#pragma omp for schedule(dynamic, 4096)
+    for (int64_t r = 0; r < nr; ++r) {
+      copies_of(rows[r], cps);
+      cols.clear();
+      cols.push_back(row_gid(rows[r]));
+      for (auto& cpy : cps) {
+        for (int w = 0; w < 15; ++w) {
+          if (w == kMC) continue;
+          int i = cpy[1] + kDirHost[w][0], j = cpy[2] + kDirHost[w][1], k = cpy[3] + kDirHost[w][2];
+          if (i < 0 || j < 0 || k < 0 || i + j + k > N) continue;
+          int64_t gj = node_gid(g, c->topo[cpy[0]], i, j, k);
+          if (is_dir(gj)) continue;
+          if (std::find(cols.begin(), cols.end(), gj) == cols.end()) cols.push_back(gj);
+        }
+      }
+      rp[r + 1] = cols.size();
+      cp[r + 1] = cps.size();
+    }
+  }
+  for (int64_t r = 0; r < nr; ++r) {
+    rp[r + 1] += rp[r];
+    cp[r + 1] += cp[r];
+  }
+  lv.nnz = (int64_t)rp[nr];
+  lv.n_copies = (int64_t)cp[nr];
+  std::vector<uint32_t> col(lv.nnz), copy(lv.n_copies);
+  std::vector<int64_t> rgid(nr);
+  std::vector<uint8_t> cmap(lv.n_copies * 16, 255);
+  bool overflow = false;
+#pragma omp parallel
+  {
+    std::vector<std::array<int, 4>> cps;
+    std::vector<int64_t> cols;
+#pragma omp for schedule(dynamic, 4096)
+    for (int64_t r = 0; r < nr; ++r) {
+      copies_of(rows[r], cps);
+      cols.clear();
+      rgid[r] = row_gid(rows[r]);
+      cols.push_back(rgid[r]);
+      uint64_t e0 = rp[r];
+      col[e0] = (uint32_t)slot_of(cps[0][0], cps[0][1], cps[0][2], cps[0][3]);
+      for (size_t q = 0; q < cps.size(); ++q) {
+        auto& cpy = cps[q];
+        uint64_t ci = cp[r] + q;
+        copy[ci] = (uint32_t)slot_of(cpy[0], cpy[1], cpy[2], cpy[3]);
+        cmap[ci * 16 + kMC] = 0;
+        for (int w = 0; w < 15; ++w) {
+          if (w == kMC) continue;
+          int i = cpy[1] + kDirHost[w][0], j = cpy[2] + kDirHost[w][1], k = cpy[3] + kDirHost[w][2];
+          if (i < 0 || j < 0 || k < 0 || i + j + k > N) continue;
+          int64_t gj = node_gid(g, c->topo[cpy[0]], i, j, k);
+          if (is_dir(gj)) continue;
+          auto it = std::find(cols.begin(), cols.end(), gj);
+          size_t pos = it - cols.begin();
+          if (it == cols.end()) {
+            cols.push_back(gj);
+            col[e0 + pos] = (uint32_t)slot_of(cpy[0], i, j, k);
+          }
+          if (pos > 250) overflow = true;
+          cmap[ci * 16 + w] = (uint8_t)pos;
+        }
+      }
+    }
+  }
+  if (overflow) return set_err(c, HHG_ERR_MESH, "lower-primitive row with more than 250 neighbours");
+
+  // ---- Dirichlet slots
+  std::vector<uint32_t> dslot;
+  std::vector<int64_t> dgid;
+  {
+    std::vector<std::array<int, 4>> cps;
+    for (auto& r : drows) {
+      copies_of(r, cps);
+      int64_t gg = row_gid(r);
+      for (auto& cpy : cps) {
+        dslot.push_back((uint32_t)slot_of(cpy[0], cpy[1], cpy[2], cpy[3]));
+        dgid.push_back(gg);
+      }
+    }
+  }
+  lv.n_dir = (int64_t)dslot.size();
+
+  // ---- upload
+  auto up = [&](auto*& dptr, const auto& vec) -> hhg_status {
+    using T = typename std::remove_reference<decltype(vec)>::type::value_type;
+    size_t bytes = std::max<size_t>(vec.size(), 1) * sizeof(T);
+    HHG_CK(c, cudaMalloc((void**)&dptr, bytes));
+    if (!vec.empty())
+      HHG_CK(c, cudaMemcpy(dptr, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return HHG_OK;
+  };
+  hhg_status st;
+  if ((st = up(lv.d_row_ptr, rp)) != HHG_OK) return st;
+  if ((st = up(lv.d_col, col)) != HHG_OK) return st;
+  if ((st = up(lv.d_copy_ptr, cp)) != HHG_OK) return st;
+  if ((st = up(lv.d_copy, copy)) != HHG_OK) return st;
+  if ((st = up(lv.d_row_gid, rgid)) != HHG_OK) return st;
+  if ((st = up(lv.d_dir_slot, dslot)) != HHG_OK) return st;
+  if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
+  HHG_CK(c, cudaMalloc(&lv.d_val, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&lv.d_val_cons, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&lv.d_tmp, std::max<int64_t>(nr, 1) * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&lv.d_cons, c->nt_local * 15 * sizeof(double)));
+  if ((st = build_lp_values(c, lv, cmap)) != HHG_OK) return st;
+  // constant (affine) stencil per macro: interior node (1,1,1)
+  {
+    std::vector<uint32_t> sl(c->nt_local);
+    for (int64_t T = 0; T < c->nt_local; ++T) sl[T] = (uint32_t)slot_of((int)T, 1, 1, 1);
+    uint32_t* d_sl = nullptr;
+    if ((st = up(d_sl, sl)) != HHG_OK) return st;
+    if ((st = launch_fem_partial(c, L, d_sl, c->nt_local, false, lv.d_cons)) != HHG_OK) return st;
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(d_sl);
+  }
+  return HHG_OK;
+}
+
+static void free_level(Level& lv) {
+  void* ps[] = {lv.d_row_ptr, lv.d_col, lv.d_val, lv.d_val_cons, lv.d_copy_ptr, lv.d_copy,
+                lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons};
+  for (void* p : ps)
+    if (p) cudaFree(p);
+  lv = Level();
+}
+
+}  // namespace hhg
+
+using namespace hhg;
+
+extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double* vertex_radius,
+                                           int64_t nv, const int64_t* tets, int64_t nt,
+                                           const uint8_t* dirichlet_face, int L_max,
+                                           const int32_t* macro_owner, int rank, int nranks,
+                                           const void* nccl_unique_id, void* cuda_stream,
+                                           hhg_ctx* out) {
+  if (!out) return HHG_ERR_INVALID;
+  *out = nullptr;
+  if (!vertices || !tets || !dirichlet_face || nv < 4 || nt < 1 || L_max < 2 || L_max > 8)
+    return HHG_ERR_INVALID;
+  if (nranks != 1 || rank != 0) return HHG_ERR_INVALID;  // multi-rank: see DESIGN.md (next round)
+  (void)nccl_unique_id;
+  (void)macro_owner;
+  Ctx* c = new Ctx();
+  c->stream = (cudaStream_t)cuda_stream;
+  c->rank = rank;
+  c->nranks = nranks;
+  c->L_max = L_max;
+  c->nv = nv;
+  c->nt = nt;
+  c->blended = vertex_radius != nullptr;
+  c->vertices.assign(vertices, vertices + 3 * nv);
+  if (vertex_radius) c->radius.assign(vertex_radius, vertex_radius + nv);
+  c->tets.assign(tets, tets + 4 * nt);
+  c->dirichlet.assign(dirichlet_face, dirichlet_face + 4 * nt);
+  auto fail = [&](hhg_status s, const std::string& m) {
+    // keep the ctx so hhg_last_error works? ABI: out = NULL on failure.
+    fprintf(stderr, "hhg_setup_macro_mesh: %s\n", m.c_str());
+    delete c;
+    return s;
+  };
+  // ---- validation
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t* tv = &tets[4 * t];
+    for (int a = 0; a < 4; ++a) {
+      if (tv[a] < 0 || tv[a] >= nv) return fail(HHG_ERR_MESH, "vertex id out of range");
+      for (int b = a + 1; b < 4; ++b)
+        if (tv[a] == tv[b]) return fail(HHG_ERR_MESH, "repeated vertex in tet");
+    }
+    double e[3][3], scale = 0.0;
+    for (int a = 0; a < 3; ++a)
+      for (int d = 0; d < 3; ++d) {
+        e[a][d] = vertices[3 * tv[a + 1] + d] - vertices[3 * tv[0] + d];
+        scale = std::max(scale, std::fabs(e[a][d]));
+      }
+    double det = e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) -
+                 e[0][1] * (e[1][0] * e[2][2] - e[1][2] * e[2][0]) +
+                 e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+    if (!(std::fabs(det) > 1e-12 * scale * scale * scale))
+      return fail(HHG_ERR_MESH, "degenerate tet " + std::to_string(t));
+  }
+  if (vertex_radius) {
+    for (int64_t v = 0; v < nv; ++v) {
+      double n = std::sqrt(vertices[3 * v] * vertices[3 * v] + vertices[3 * v + 1] * vertices[3 * v + 1] +
+                           vertices[3 * v + 2] * vertices[3 * v + 2]);
+      if (!(vertex_radius[v] > 0) || std::fabs(n - vertex_radius[v]) > 1e-12 * vertex_radius[v])
+        return fail(HHG_ERR_MESH, "|x_v| != r_v at vertex " + std::to_string(v));
+    }
+  }
+  // ---- topology
+  Topology tp;
+  std::vector<int64_t> ek, fk;
+  ek.reserve(6 * nt);
+  fk.reserve(4 * nt);
+  for (int64_t t = 0; t < nt; ++t) {
+    int64_t s[4];
+    for (int a = 0; a < 4; ++a) s[a] = tets[4 * t + a];
+    std::sort(s, s + 4);
+    for (int a = 0; a < 4; ++a)
+      for (int b = a + 1; b < 4; ++b) ek.push_back(s[a] * nv + s[b]);
+    for (int f = 0; f < 4; ++f) {
+      int64_t q[3];
+      int n = 0;
+      for (int a = 0; a < 4; ++a)
+        if (a != f) q[n++] = s[a];
+      fk.push_back((q[0] * nv + q[1]) * nv + q[2]);
+    }
+  }
+  std::sort(ek.begin(), ek.end());
+  ek.erase(std::unique(ek.begin(), ek.end()), ek.end());
+  std::sort(fk.begin(), fk.end());
+  fk.erase(std::unique(fk.begin(), fk.end()), fk.end());
+  tp.ekey = ek;
+  tp.fkey = fk;
+  c->n_e = (int64_t)ek.size();
+  c->n_f = (int64_t)fk.size();
+  // local macros (single rank: all)
+  c->nt_local = nt;
+  c->local_macros.resize(nt);
+  std::iota(c->local_macros.begin(), c->local_macros.end(), 0);
+  c->topo.resize(c->nt_local);
+  tp.vinc.assign(nv, {});
+  tp.einc.assign(c->n_e, {});
+  tp.finc.assign(c->n_f, {});
+  tp.vdir.assign(nv, 0);
+  tp.edir.assign(c->n_e, 0);
+  tp.fdir.assign(c->n_f, 0);
+  for (int64_t T = 0; T < c->nt_local; ++T) {
+    int64_t t = c->local_macros[T];
+    MacroTopo& m = c->topo[T];
+    m.gT = t;
+    for (int a = 0; a < 4; ++a) m.gv[a] = tets[4 * t + a];
+    for (int a = 0; a < 4; ++a)
+      for (int b = a + 1; b < 4; ++b) {
+        int64_t x = std::min(m.gv[a], m.gv[b]), y = std::max(m.gv[a], m.gv[b]);
+        m.e[local_edge(a, b)] = std::lower_bound(ek.begin(), ek.end(), x * nv + y) - ek.begin();
+      }
+    for (int f = 0; f < 4; ++f) {
+      int64_t q[3];
+      int n = 0;
+      for (int a = 0; a < 4; ++a)
+        if (a != f) q[n++] = m.gv[a];
+      std::sort(q, q + 3);
+      m.f[f] = std::lower_bound(fk.begin(), fk.end(), (q[0] * nv + q[1]) * nv + q[2]) - fk.begin();
+    }
+    for (int a = 0; a < 4; ++a) tp.vinc[m.gv[a]].push_back((int32_t)T);
+    for (int e = 0; e < 6; ++e) tp.einc[m.e[e]].push_back((int32_t)T);
+    for (int f = 0; f < 4; ++f) tp.finc[m.f[f]].push_back((int32_t)T);
+  }
+  for (int64_t f = 0; f < c->n_f; ++f)
+    if (tp.finc[f].size() > 2) return fail(HHG_ERR_MESH, "face shared by more than two tets");
+  // Dirichlet closure
+  for (int64_t T = 0; T < c->nt_local; ++T) {
+    const MacroTopo& m = c->topo[T];
+    for (int f = 0; f < 4; ++f) {
+      if (!dirichlet_face[4 * m.gT + f]) continue;
+      tp.fdir[m.f[f]] = 1;
+      for (int a = 0; a < 4; ++a) {
+        if (a == f) continue;
+        tp.vdir[m.gv[a]] = 1;
+        for (int b = a + 1; b < 4; ++b)
+          if (b != f) tp.edir[m.e[local_edge(a, b)]] = 1;
+      }
+    }
+  }
+  // ---- device geometry
+  std::vector<double> geo(c->nt_local * 16);
+  for (int64_t T = 0; T < c->nt_local; ++T)
+    for (int a = 0; a < 4; ++a) {
+      int64_t v = c->topo[T].gv[a];
+      for (int d = 0; d < 3; ++d) geo[T * 16 + 4 * a + d] = vertices[3 * v + d];
+      geo[T * 16 + 4 * a + 3] = vertex_radius ? vertex_radius[v] : 0.0;
+    }
+  cudaError_t e1 = cudaMalloc(&c->d_geo, geo.size() * sizeof(double));
+  if (e1 != cudaSuccess) return fail(HHG_ERR_CUDA, cudaGetErrorString(e1));
+  cudaMemcpy(c->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMalloc(&c->d_topo, c->topo.size() * sizeof(MacroTopo));
+  cudaMemcpy(c->d_topo, c->topo.data(), c->topo.size() * sizeof(MacroTopo), cudaMemcpyHostToDevice);
+  c->levels.resize(L_max + 1);
+  for (int L = 2; L <= L_max; ++L) {
+    hhg_status st = build_level(c, tp, L);
+    if (st != HHG_OK) {
+      std::string m = c->err;
+      hhg_destroy((hhg_ctx)c);
+      fprintf(stderr, "hhg_setup_macro_mesh: level %d: %s\n", L, m.c_str());
+      return st;
+    }
+  }
+  *out = (hhg_ctx)c;
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_vector_layout(hhg_ctx ctx, int L, int64_t* n_local, int64_t* n_owned,
+                                        int64_t* n_global) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || L < 2 || L > c->L_max) return HHG_ERR_INVALID;
+  const Level& lv = c->levels[L];
+  if (n_local) *n_local = lv.n_local;
+  if (n_owned) *n_owned = lv.n_owned;
+  if (n_global) *n_global = lv.gi.n_total;
+  return HHG_OK;
+}
+
+extern "C" const char* hhg_last_error(hhg_ctx ctx) {
+  Ctx* c = (Ctx*)ctx;
+  return c ? c->err.c_str() : "null ctx";
+}
+
+extern "C" int64_t hhg_kernel_launches(hhg_ctx ctx) {
+  Ctx* c = (Ctx*)ctx;
+  return c ? c->launches : -1;
+}
+
+extern "C" void hhg_destroy(hhg_ctx ctx) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c) return;
+  cudaStreamSynchronize(c->stream);
+  for (auto& lv : c->levels) free_level(lv);
+  if (c->d_geo) cudaFree(c->d_geo);
+  if (c->d_topo) cudaFree(c->d_topo);
+  for (auto* p : c->d_stage)
+    if (p) cudaFree(p);
+  if (c->d_red) cudaFree(c->d_red);
+  if (c->h_red) cudaFreeHost(c->h_red);
+  delete c;
+}
