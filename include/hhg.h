@@ -175,6 +175,14 @@ hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t macro, doubl
 /* Count of this library's kernel launches since setup (for the bench). */
 int64_t hhg_kernel_launches(hhg_ctx ctx);
 
+/* Per-kernel device timing for the bench: while enabled, every launch of a
+ * kernel class is bracketed by CUDA events on the ctx stream.  kind: 0 =
+ * volume apply/residual kernels, 1 = volume GS kernels, 2 = lower-primitive
+ * row kernels, 3 = everything else.  hhg_profile_read synchronises, returns
+ * the summed device time (ms) and launch count of `kind`, and clears it. */
+hhg_status hhg_profile(hhg_ctx ctx, int enable);
+hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, int64_t* launches);
+
 const char* hhg_last_error(hhg_ctx ctx);
 void hhg_destroy(hhg_ctx ctx);
 

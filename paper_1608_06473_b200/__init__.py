@@ -50,6 +50,10 @@ def lib():
     L.hhg_scatter_global.argtypes = [P, I32, P, P]
     L.hhg_sync_copies.argtypes = [P, I32, P]
     L.hhg_eval_stencils.argtypes = [P, I32, I32, I64, P]
+    L.hhg_profile.argtypes = [P, I32]
+    L.hhg_profile.restype = ctypes.c_int
+    L.hhg_profile_read.argtypes = [P, I32, ctypes.POINTER(D), ctypes.POINTER(I64)]
+    L.hhg_profile_read.restype = ctypes.c_int
     L.hhg_kernel_launches.argtypes = [P]
     L.hhg_kernel_launches.restype = I64
     L.hhg_last_error.argtypes = [P]
@@ -194,3 +198,15 @@ class Ctx:
     @property
     def kernel_launches(self):
         return int(self._lib.hhg_kernel_launches(self.h))
+
+    def profile(self, enable=True):
+        self._check(self._lib.hhg_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{class: (total device ms, launches)} since the last read; clears."""
+        out = {}
+        for k, name in enumerate(("vol_apply", "vol_gs", "lp_rows", "other")):
+            ms, n = ctypes.c_double(), ctypes.c_int64()
+            self._check(self._lib.hhg_profile_read(self.h, k, ctypes.byref(ms), ctypes.byref(n)))
+            out[name] = (ms.value, n.value)
+        return out

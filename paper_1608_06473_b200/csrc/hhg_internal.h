@@ -156,6 +156,38 @@ struct Ctx {
   double* d_red = nullptr;            // reduction scratch
   double* h_red = nullptr;            // pinned
   int64_t red_n = 0;
+  // profiling (hhg_profile)
+  bool prof = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_rec[4];
+};
+
+// RAII event bracket around kernel launches of class `kind` (no-op unless profiling)
+struct ProfScope {
+  Ctx* c;
+  int kind;
+  cudaEvent_t a = nullptr, b = nullptr;
+  static cudaEvent_t get(Ctx* c) {
+    if (!c->ev_pool.empty()) {
+      cudaEvent_t e = c->ev_pool.back();
+      c->ev_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  ProfScope(Ctx* c_, int k) : c(c_), kind(k) {
+    if (!c->prof) return;
+    a = get(c);
+    b = get(c);
+    cudaEventRecord(a, c->stream);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, c->stream);
+    c->ev_rec[kind].push_back({a, b});
+  }
 };
 
 // error helpers ------------------------------------------------------------

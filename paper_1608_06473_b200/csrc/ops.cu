@@ -214,6 +214,7 @@ static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
                               const double* f, double* out) {
   dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
+  ProfScope ps(c, mode == kModeGS ? 1 : 0);
   k_vol_v1<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_geo, lv.d_coef, lv.mq, lv.d_cons, op,
                                         c->blended, mode, colour, u, f, out);
   HHG_LAUNCHED(c);
@@ -224,6 +225,7 @@ static hhg_status lp_pass(Ctx* c, Level& lv, int op, int mode, const double* u, 
                           double* out) {
   if (lv.n_rows == 0) return HHG_OK;
   const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_val_cons : lv.d_val;
+  ProfScope ps(c, 2);
   k_lp_apply<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(0, lv.n_rows, lv.d_row_ptr, lv.d_col, val,
                                                          lv.d_copy_ptr, lv.d_copy, u, f, out, mode);
   HHG_LAUNCHED(c);
@@ -232,6 +234,7 @@ static hhg_status lp_pass(Ctx* c, Level& lv, int op, int mode, const double* u, 
 
 static hhg_status zero_dir(Ctx* c, Level& lv, double* out) {
   if (lv.n_dir == 0) return HHG_OK;
+  ProfScope ps(c, 3);
   k_zero_slots<<<nblk(lv.n_dir, 256), 256, 0, c->stream>>>(lv.n_dir, lv.d_dir_slot, out);
   HHG_LAUNCHED(c);
   return HHG_OK;
@@ -259,6 +262,7 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
   for (int s = 0; s < kNumLpSteps; ++s) {
     int64_t r0 = lv.step_start[s], r1 = lv.step_start[s + 1];
     if (r1 <= r0) continue;
+    ProfScope ps(c, 2);
     k_lp_gs_compute<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_row_ptr, lv.d_col, val, u, f,
                                                                lv.d_tmp);
     HHG_LAUNCHED(c);
@@ -420,5 +424,30 @@ extern "C" hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t m
     HHG_CK(c, cudaMemcpyAsync(out, so.dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     HHG_CK(c, cudaStreamSynchronize(c->stream));
   }
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_profile(hhg_ctx ctx, int enable) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c) return HHG_ERR_INVALID;
+  c->prof = enable != 0;
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, int64_t* launches) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || kind < 0 || kind > 3) return HHG_ERR_INVALID;
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  double tot = 0.0;
+  for (auto& p : c->ev_rec[kind]) {
+    float ms = 0.f;
+    HHG_CK(c, cudaEventElapsedTime(&ms, p.first, p.second));
+    tot += ms;
+    c->ev_pool.push_back(p.first);
+    c->ev_pool.push_back(p.second);
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (int64_t)c->ev_rec[kind].size();
+  c->ev_rec[kind].clear();
   return HHG_OK;
 }

@@ -507,5 +507,11 @@ extern "C" void hhg_destroy(hhg_ctx ctx) {
     if (p) cudaFree(p);
   if (c->d_red) cudaFree(c->d_red);
   if (c->h_red) cudaFreeHost(c->h_red);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  for (auto& v : c->ev_rec)
+    for (auto& p : v) {
+      cudaEventDestroy(p.first);
+      cudaEventDestroy(p.second);
+    }
   delete c;
 }
