@@ -121,6 +121,18 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
   const int mq = n_coeffs(q);
   std::vector<int> el, em, en;
   exponents(q, el, em, en);
+  // q <= 2: the march kernels read coefficients zero-padded to the q = 2 layout
+  // (the degree-major exponent list of q is a prefix of that of q = 2).
+  auto make10 = [&](Level& lv) -> hhg_status {
+    if (lv.d_coef10) cudaFree(lv.d_coef10);
+    lv.d_coef10 = nullptr;
+    if (q > 2) return HHG_OK;
+    HHG_CK(c, cudaMalloc(&lv.d_coef10, c->nt_local * 150 * sizeof(double)));
+    HHG_CK(c, cudaMemsetAsync(lv.d_coef10, 0, c->nt_local * 150 * sizeof(double), c->stream));
+    HHG_CK(c, cudaMemcpy2DAsync(lv.d_coef10, 10 * sizeof(double), lv.d_coef, mq * sizeof(double),
+                                mq * sizeof(double), c->nt_local * 15, cudaMemcpyDeviceToDevice, c->stream));
+    return HHG_OK;
+  };
   for (int L = 2; L <= c->L_max; ++L) {
     Level& lv = c->levels[L];
     const int N = lv.N;
@@ -132,6 +144,8 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
     if (L == 2) {
       k_exact_const<<<(unsigned)c->nt_local, 32, 0, c->stream>>>(c->d_geo, N, mq, c->blended, lv.d_coef);
       HHG_LAUNCHED(c);
+      hhg_status st2 = make10(lv);
+      if (st2 != HHG_OK) return st2;
       lv.fitted = true;
       continue;
     }
@@ -189,7 +203,10 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
     cudaFree(d_pinv);
     cudaFree(d_B);
     cudaFree(d_scale);
+    hhg_status st2 = make10(lv);
+    if (st2 != HHG_OK) return st2;
     lv.fitted = true;
   }
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
   return HHG_OK;
 }

@@ -99,6 +99,17 @@ __host__ __device__ inline int64_t node_gid(const GidInfo& g, const MacroTopo& t
   return g.base_v + t.gT * g.nvi + vol_index(N, i, j, k);
 }
 
+// Band of diagonals handled by one CTA of the column-march kernels (march.cuh).
+struct Band {
+  int d0, d1;       // diagonals [d0, d1) computed by this band
+  int c_lo;         // first column index loaded (diagonal d0-1, j=0)
+  int ncols;        // columns loaded per plane (diagonals d0-1 .. d1)
+  int kmax;         // last plane computed (N-1-d0)
+  int ncolumns;     // interior columns (threads used)
+};
+constexpr int kMarchThreads = 256;
+constexpr int kRing = 16;  // plane slots (power of 2); >= 11 planes in flight ahead of use
+
 // ---------------------------------------------------------------------------
 // Per-level state
 // ---------------------------------------------------------------------------
@@ -129,7 +140,12 @@ struct Level {
   int mq = 0;
   double* d_coef = nullptr;        // [nt_local][15][mq] index units, exponent order kExp
   double* d_cons = nullptr;        // [nt_local][15] affine constant stencil
+  double* d_coef10 = nullptr;      // [nt_local][15][10] q<=2 coefficients zero-padded to q=2
   bool fitted = false;
+  // column-march bands
+  std::vector<Band> bands;
+  Band* d_bands = nullptr;
+  int slot_len = 0;
 };
 
 struct Ctx {

@@ -1,0 +1,312 @@
+// Column-march volume kernels (apply / residual / GS colour pass) -- the
+// surrogate hot path.
+//
+// Layout (include/hhg.h): pos(i,j,k) = planeoff(k) + col(i,j), col(i,j) =
+// d(d+1)/2 + j with d = i+j, so a lattice column (i,j) has the SAME column
+// index in every plane and plane k is the prefix col < (N-k+1)(N-k+2)/2.
+//
+// One CTA = (macro, band of diagonals [d0,d1)), one thread = one interior
+// column (i,j), marching in k.  The CTA needs, per plane, the diagonals
+// [d0-1, d1] only: a CONTIGUOUS range of every plane, brought into a 16-slot
+// shared-memory ring by one 1-D TMA bulk copy (cp.async.bulk + mbarrier
+// complete_tx) issued >= 8 planes ahead of use.  In plane k-1 / k / k+1 all 15
+// stencil neighbours of (i,j,k) sit at only 7 column offsets
+// (i,j) (i+1,j) (i,j+1) (i-1,j+1) (i-1,j) (i,j-1) (i+1,j-1).
+//
+// Stencil weights (fix two indices, evaluate a 1-D
+// polynomial incrementally): for q <= 2 the surrogate polynomial restricted to
+// column (i,j) is s_w(k) = A_w + B_w k + C_w k^2; A_w, B_w are computed once
+// per column (registers) from the macro's coefficients and C_w = c_002 is per
+// macro (shared memory, broadcast), so each weight costs 2 DFMA per node
+// (Horner in k) and the stencil 15 more: 45 DFMA per unknown (Table flops
+// "29+15q" counts the same work).  f and the output are
+// read/written straight from/to HBM: consecutive threads own consecutive
+// columns => coalesced (apply) or 1 double per sector per colour (GS).
+#pragma once
+#include "hhg_internal.h"
+
+namespace hhg {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Issue the bulk copy of plane p's band range into ring slot p % kRing.
+__device__ __forceinline__ void issue_plane(const double* ub, int N, int p, const Band& b, double* ring,
+                                            int slot_len, uint64_t* bars) {
+  const int64_t g0 = plane_off(N, p) + b.c_lo;
+  const int64_t a0 = g0 & ~(int64_t)1;
+  const int64_t a1 = (g0 + b.ncols + 1) & ~(int64_t)1;
+  const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
+  const int s = p & (kRing - 1);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(&bars[s], bytes);
+  tma_load_1d(ring + s * slot_len, ub + a0, bytes, &bars[s]);
+}
+
+// Shared-memory carve-up common to the march kernels.
+struct MarchSmem {
+  double* ring;     // [kRing][slot_len]
+  uint64_t* bars;   // [kRing]
+  double* Cw;       // [16] k^2 coefficients of the 15 weights (per macro)
+  int* po;          // [N+2] plane offsets
+  __device__ MarchSmem(double* smem, int slot_len) {
+    ring = smem;
+    bars = (uint64_t*)(smem + kRing * slot_len);
+    Cw = (double*)(bars + kRing);
+    po = (int*)(Cw + 16);
+  }
+};
+
+__host__ __device__ inline size_t march_smem_bytes(int slot_len, int N) {
+  return (size_t)kRing * slot_len * 8 + kRing * 8 + 16 * 8 + (size_t)(N + 2) * 4;
+}
+
+struct Column {
+  bool active;
+  int i, j, d, len, c;
+  int o_c, o_e, o_n, o_nw, o_w, o_s, o_se;  // ring offsets of (i,j)(i+1,j)(i,j+1)(i-1,j+1)(i-1,j)(i,j-1)(i+1,j-1)
+};
+
+__device__ __forceinline__ Column make_column(const Band& b, int N) {
+  Column q;
+  int t = threadIdx.x, d = b.d0, j = 0;
+  q.active = t < b.ncolumns;
+  if (q.active) {
+    while (t >= d - 1) { t -= d - 1; ++d; }
+    j = t + 1;
+  }
+  q.d = d;
+  q.j = j;
+  q.i = d - j;
+  q.len = N - 1 - d;
+  q.c = (int)col_idx(q.i, j);
+  const int lo = b.c_lo;
+  q.o_c = q.c - lo;
+  q.o_e = (int)col_idx(q.i + 1, j) - lo;
+  q.o_n = (int)col_idx(q.i, j + 1) - lo;
+  q.o_nw = (int)col_idx(q.i - 1, j + 1) - lo;
+  q.o_w = (int)col_idx(q.i - 1, j) - lo;
+  q.o_s = (int)col_idx(q.i, j - 1) - lo;
+  q.o_se = (int)col_idx(q.i + 1, j - 1) - lo;
+  return q;
+}
+
+// A_w, B_w of the column's 1-D polynomial s_w(k) = A_w + B_w k + C_w k^2.
+template <int OP>
+__device__ __forceinline__ void column_coeffs(const double* coef10, const double* cons, int64_t T, int i, int j,
+                                              double A[15], double B[15]) {
+  if (OP == HHG_OP_SURROGATE) {
+    const double* a = coef10 + T * 150;
+    const double di = (double)i, dj = (double)j;
+#pragma unroll
+    for (int w = 0; w < 15; ++w) {
+      const double* q = a + w * 10;  // (000)(100)(010)(001)(200)(110)(101)(020)(011)(002)
+      A[w] = q[0] + di * (q[1] + di * q[4] + dj * q[5]) + dj * (q[2] + dj * q[7]);
+      B[w] = q[3] + di * q[6] + dj * q[8];
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < 15; ++w) {
+      A[w] = cons[T * 15 + w];
+      B[w] = 0.0;
+    }
+  }
+}
+
+__device__ __forceinline__ void march_prologue(MarchSmem& sm, const Band& b, int N, const double* coef10,
+                                               int64_t T, int op) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(&sm.bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 15) sm.Cw[threadIdx.x] = (op == HHG_OP_SURROGATE) ? coef10[T * 150 + threadIdx.x * 10 + 9] : 0.0;
+  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) sm.po[p] = (int)plane_off(N, p);
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// apply / residual: march k = 1..len, one node per step, 7 new shared loads
+// ---------------------------------------------------------------------------
+template <int OP, int MODE>
+__global__ void __launch_bounds__(kMarchThreads, 2)
+    k_vol_march(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
+                const double* __restrict__ coef10, const double* __restrict__ cons,
+                const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out) {
+  extern __shared__ __align__(16) double smem[];
+  MarchSmem sm(smem, slot_len);
+  const int64_t T = blockIdx.x / n_bands;
+  const Band b = bands[blockIdx.x - T * n_bands];
+  const double* ub = u + T * S;
+  const Column q = make_column(b, N);
+  double A[15], B[15];
+  column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
+  march_prologue(sm, b, N, coef10, T, OP);
+
+  const int last_plane = b.kmax + 1;
+  int next_issue = kRing;  // thread 0 only
+  if (threadIdx.x == 0)
+    for (int p = 0; p < kRing && p <= last_plane; ++p) issue_plane(ub, N, p, b, sm.ring, slot_len, sm.bars);
+
+  const int clo = b.c_lo;
+  auto sptr = [&](int p, int pof) -> const double* {
+    return sm.ring + (p & (kRing - 1)) * slot_len + ((pof + clo) & 1);
+  };
+  int po1 = sm.po[1];
+  mbar_wait(&sm.bars[0], 0);
+  mbar_wait(&sm.bars[1], 0);
+  double bc, be, bn, bnw, mc, mw, ms, mse;
+  {
+    const double* P0 = sptr(0, 0);
+    const double* P1 = sptr(1, po1);
+    bc = P0[q.o_c]; be = P0[q.o_e]; bn = P0[q.o_n]; bnw = P0[q.o_nw];
+    mc = P1[q.o_c]; mw = P1[q.o_w]; ms = P1[q.o_s]; mse = P1[q.o_se];
+  }
+  double* const optr = out + T * S + q.c;
+  const double* const fptr = f + T * S + q.c;
+  for (int k = 1; k <= b.kmax; ++k) {
+    const int po2 = sm.po[k + 1];
+    mbar_wait(&sm.bars[(k + 1) & (kRing - 1)], ((k + 1) / kRing) & 1);
+    if (q.active && k <= q.len) {
+      const double* Pk = sptr(k, po1);
+      const double* Pk1 = sptr(k + 1, po2);
+      const double me = Pk[q.o_e], mn = Pk[q.o_n], mnw = Pk[q.o_nw];
+      const double tc = Pk1[q.o_c], tw = Pk1[q.o_w], ts = Pk1[q.o_s], tse = Pk1[q.o_se];
+      const double uu[15] = {bc, be, bn, bnw, ms, mse, mw, mc, me, mnw, mn, tse, ts, tw, tc};
+      double fv = 0.0;
+      if (MODE == kModeResid) fv = __ldg(fptr + po1);
+      double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      if (OP == HHG_OP_SURROGATE) {
+        const double kd = (double)k;
+#pragma unroll
+        for (int w = 0; w < 15; ++w) {
+          const double s = fma(fma(sm.Cw[w], kd, B[w]), kd, A[w]);
+          acc[w % 5] = fma(s, uu[w], acc[w % 5]);
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < 15; ++w) acc[w % 5] = fma(A[w], uu[w], acc[w % 5]);
+      }
+      const double r = (acc[0] + acc[1]) + (acc[2] + acc[3]) + acc[4];
+      optr[po1] = (MODE == kModeResid) ? fv - r : r;
+      bc = mc; mc = tc; be = me; bn = mn; bnw = mnw; mw = tw; ms = ts; mse = tse;
+    }
+    po1 = po2;
+    // every 8 steps: all warps are done with planes <= k; refill their slots.
+    // Warps drift freely between these barriers (ring of 16 keeps >= 8 planes ahead).
+    if ((k & 7) == 0) {
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (; next_issue <= k + kRing && next_issue <= last_plane; ++next_issue)
+          issue_plane(ub, N, next_issue, b, sm.ring, slot_len, sm.bars);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GS colour pass: every node of colour c = (i+2j+3k) mod 4 of the band, in
+// place (eq. iteration-scheme).  Nodes of one colour are
+// never neighbours (R14), so the pass is order-free; each thread
+// visits its colour-c nodes k = delta + 4s (one per step of 4 planes).
+// ---------------------------------------------------------------------------
+template <int OP>
+__global__ void __launch_bounds__(kMarchThreads, 2)
+    k_gs_march(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
+               const double* __restrict__ coef10, const double* __restrict__ cons, int colour,
+               double* __restrict__ u, const double* __restrict__ f) {
+  extern __shared__ __align__(16) double smem[];
+  MarchSmem sm(smem, slot_len);
+  const int64_t T = blockIdx.x / n_bands;
+  const Band b = bands[blockIdx.x - T * n_bands];
+  double* ub = u + T * S;
+  const Column q = make_column(b, N);
+  double A[15], B[15];
+  column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
+  march_prologue(sm, b, N, coef10, T, OP);
+  // colour(i,j,k) = (d + j + 3k) mod 4 == colour  <=>  k == 3 (colour - d - j) mod 4
+  const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
+
+  const int last_plane = b.kmax + 1;
+  int next_issue = kRing;
+  if (threadIdx.x == 0)
+    for (int p = 0; p < kRing && p <= last_plane; ++p) issue_plane(ub, N, p, b, sm.ring, slot_len, sm.bars);
+  const int clo = b.c_lo;
+  auto sptr = [&](int p) -> const double* {
+    return sm.ring + (p & (kRing - 1)) * slot_len + ((sm.po[p] + clo) & 1);
+  };
+  const double* const fb = f + T * S + q.c;
+  double* const wb = ub + q.c;
+  int waited = -1;  // planes <= waited are resident
+  const int nsteps = (b.kmax + 4) / 4;
+  for (int s = 0; s < nsteps; ++s) {
+    const int top = min(4 * s + 4, last_plane);
+    for (int p = waited + 1; p <= top; ++p) mbar_wait(&sm.bars[p & (kRing - 1)], (p / kRing) & 1);
+    waited = top;
+    const int k = 4 * s + delta;
+    if (q.active && k >= 1 && k <= q.len) {
+      const double* Pb = sptr(k - 1);
+      const double* Pm = sptr(k);
+      const double* Pt = sptr(k + 1);
+      const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
+                             Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
+                             Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
+      const int pk = sm.po[k];
+      const double fv = __ldg(fb + pk);
+      double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      double smc;
+      if (OP == HHG_OP_SURROGATE) {
+        const double kd = (double)k;
+#pragma unroll
+        for (int w = 0; w < 15; ++w) {
+          const double sw = fma(fma(sm.Cw[w], kd, B[w]), kd, A[w]);
+          if (w == kMC) smc = sw;
+          else acc[w % 5] = fma(sw, uu[w], acc[w % 5]);
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < 15; ++w) {
+          if (w == kMC) smc = A[w];
+          else acc[w % 5] = fma(A[w], uu[w], acc[w % 5]);
+        }
+      }
+      const double r = (acc[0] + acc[1]) + (acc[2] + acc[3]) + acc[4];
+      wb[pk] = (fv - r) / smc;
+    }
+    // all warps done with planes <= 4s+2 (next step reads >= 4s+3)
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (; next_issue <= 4 * s + 2 + kRing && next_issue <= last_plane; ++next_issue)
+        issue_plane(ub, N, next_issue, b, sm.ring, slot_len, sm.bars);
+  }
+}
+
+}  // namespace hhg

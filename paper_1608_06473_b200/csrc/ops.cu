@@ -10,6 +10,7 @@
 #include "fem_device.cuh"
 #include "hhg_internal.h"
 #include "vol_kernels.cuh"
+#include "march.cuh"
 
 namespace hhg {
 
@@ -211,8 +212,63 @@ static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
 }
 
 // The volume pass of one operation (apply / residual / GS colour).
+static bool force_v1() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HHG_VOLUME_KERNEL");
+    v = (e && std::string(e) == "v1") ? 1 : 0;
+  }
+  return v == 1;
+}
+
+template <int OP, int MODE>
+static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
+  const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
+  static bool attr = false;
+  if (!attr) {
+    HHG_CK(c, cudaFuncSetAttribute(k_vol_march<OP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    attr = true;
+  }
+  const int nb = (int)lv.bands.size();
+  ProfScope ps(c, 0);
+  k_vol_march<OP, MODE><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+template <int OP>
+static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, const double* f) {
+  const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
+  static bool attr = false;
+  if (!attr) {
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_march<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    attr = true;
+  }
+  const int nb = (int)lv.bands.size();
+  ProfScope ps(c, 1);
+  k_gs_march<OP><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, colour, u, f);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
                               const double* f, double* out) {
+  if (mode == kModeGS && !force_v1() && !lv.bands.empty()) {
+    if (op == HHG_OP_SURROGATE && lv.d_coef10) return launch_gs_march<HHG_OP_SURROGATE>(c, lv, colour, out, f);
+    if (op == HHG_OP_CONST_AFFINE) return launch_gs_march<HHG_OP_CONST_AFFINE>(c, lv, colour, out, f);
+  }
+  if (mode != kModeGS && !force_v1() && !lv.bands.empty()) {
+    if (op == HHG_OP_SURROGATE && lv.d_coef10) {
+      return mode == kModeApply ? launch_march<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out)
+                                : launch_march<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out);
+    }
+    if (op == HHG_OP_CONST_AFFINE) {
+      return mode == kModeApply ? launch_march<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
+                                : launch_march<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
+    }
+  }
   dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
   ProfScope ps(c, mode == kModeGS ? 1 : 0);
   k_vol_v1<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_geo, lv.d_coef, lv.mq, lv.d_cons, op,

@@ -80,7 +80,24 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   lv.L = L;
   lv.N = N;
   lv.P = n_lattice(N);
-  lv.S = (lv.P + 31) / 32 * 32;
+  lv.S = (lv.P + 2 + 31) / 32 * 32;  // >= P+2: 16-byte-rounded bulk copies stay inside the block
+  // column-march bands: consecutive diagonals with <= kMarchThreads interior columns
+  lv.bands.clear();
+  lv.slot_len = 0;
+  for (int d = 2; d <= N - 2;) {
+    Band b{};
+    b.d0 = d;
+    int cnt = 0;
+    while (d <= N - 2 && cnt + (d - 1) <= kMarchThreads) cnt += d - 1, ++d;
+    if (cnt == 0) return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA");
+    b.d1 = d;
+    b.ncolumns = cnt;
+    b.c_lo = (int)col_idx(b.d0 - 1, 0);
+    b.ncols = (int)col_idx(0, b.d1) + 1 - b.c_lo;  // through the end of diagonal d1
+    b.kmax = N - 1 - b.d0;
+    lv.bands.push_back(b);
+    lv.slot_len = std::max(lv.slot_len, (b.ncols + 2 + 3) / 4 * 4);
+  }
   lv.n_local = lv.S * c->nt_local;
   GidInfo& g = lv.gi;
   g.N = N;
@@ -283,6 +300,7 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if ((st = up(lv.d_row_gid, rgid)) != HHG_OK) return st;
   if ((st = up(lv.d_dir_slot, dslot)) != HHG_OK) return st;
   if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
+  if ((st = up(lv.d_bands, lv.bands)) != HHG_OK) return st;
   HHG_CK(c, cudaMalloc(&lv.d_val, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_val_cons, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_tmp, std::max<int64_t>(nr, 1) * sizeof(double)));
@@ -303,7 +321,8 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
 
 static void free_level(Level& lv) {
   void* ps[] = {lv.d_row_ptr, lv.d_col, lv.d_val, lv.d_val_cons, lv.d_copy_ptr, lv.d_copy,
-                lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons};
+                lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
+                lv.d_coef10, lv.d_bands};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
