@@ -1,0 +1,301 @@
+// Structured lower-primitive rows of macro faces.
+//
+// Face nodes are the bulk of the lower-primitive unknowns (PAPER.md:300-302,
+// 321-327).  Their rows are the exact FEM rows (assembled from the local
+// stiffness matrices of the 24 adjacent fine tets),
+// computed once at setup and stored as 15 doubles per row (structure-of-arrays,
+// coalesced).  Columns are NOT stored: every face node has the same neighbour
+// pattern -- centre, 6 in-face, 4 into each adjacent macro -- so the slots are
+// recomputed from (face, s, t) and the face's orientation in its two macros.
+#include "fem_device.cuh"
+#include "hhg_internal.h"
+
+namespace hhg {
+
+struct FaceNode {
+  int i, j, k;
+};
+
+__device__ __forceinline__ FaceNode face_node(const int8_t* l, int N, int s, int t) {
+  int w[4] = {0, 0, 0, 0};
+  w[l[0]] = N - s - t;
+  w[l[1]] = s;
+  w[l[2]] = t;
+  return FaceNode{w[1], w[2], w[3]};
+}
+
+__device__ __forceinline__ int64_t fslot(int64_t T, int64_t S, const int* po, int i, int j, int k) {
+  return T * S + po[k] + col_idx(i, j);
+}
+
+__global__ void k_face_values(const double* __restrict__ geo, int N, int64_t nfi, int64_t n_frows,
+                              const FaceLP* __restrict__ flp, const uint32_t* __restrict__ fst, bool blended,
+                              double* __restrict__ val) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_frows) return;
+  const int64_t f = r / nfi;
+  const uint32_t st = fst[r - f * nfi];
+  const int s = st & 0xffff, t = st >> 16;
+  const FaceLP F = flp[f];
+  double acc[15];
+  for (int e = 0; e < 15; ++e) acc[e] = 0.0;
+  for (int side = 0; side < 2; ++side) {
+    const int T = side == 0 ? F.TA : F.TB;
+    if (T < 0) continue;
+    const FaceNode n = face_node(side == 0 ? F.lA : F.lB, N, s, t);
+    double part[15];
+    fem_partial(geo + (int64_t)T * 16, N, n.i, n.j, n.k, blended, part);
+    const int8_t* map = side == 0 ? F.mapA : F.mapB;
+    for (int w = 0; w < 15; ++w)
+      if (map[w] >= 0) acc[map[w]] += part[w];
+  }
+  for (int e = 0; e < 15; ++e) val[e * n_frows + r] = acc[e];
+}
+
+hhg_status build_face_values(Ctx* c, Level& lv) {
+  if (lv.n_frows == 0) return HHG_OK;
+  const unsigned grid = (unsigned)((lv.n_frows + 127) / 128);
+  k_face_values<<<grid, 128, 0, c->stream>>>(c->d_geo, lv.N, lv.gi.nfi, lv.n_frows, lv.d_flp, lv.d_fst, true,
+                                             lv.d_fval);
+  HHG_LAUNCHED(c);
+  k_face_values<<<grid, 128, 0, c->stream>>>(c->d_geo, lv.N, lv.gi.nfi, lv.n_frows, lv.d_flp, lv.d_fst, false,
+                                             lv.d_fval_cons);
+  HHG_LAUNCHED(c);
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  return HHG_OK;
+}
+
+// Slots of one face row: centre in A (and B), 14 neighbours.
+struct FaceRowSlots {
+  int64_t cA, cB;      // centre copies (cB = -1 if none)
+  int64_t nb[14];      // neighbours for entries 1..14 (-1 if absent)
+};
+
+__device__ __forceinline__ void face_row_slots(const FaceLP& F, int N, int64_t S, const int* po, int s, int t,
+                                               FaceRowSlots& o) {
+  const FaceNode a = face_node(F.lA, N, s, t);
+  o.cA = fslot(F.TA, S, po, a.i, a.j, a.k);
+#pragma unroll
+  for (int e = 0; e < 10; ++e)
+    o.nb[e] = fslot(F.TA, S, po, a.i + F.off[e][0], a.j + F.off[e][1], a.k + F.off[e][2]);
+  if (F.TB >= 0) {
+    const FaceNode b = face_node(F.lB, N, s, t);
+    o.cB = fslot(F.TB, S, po, b.i, b.j, b.k);
+#pragma unroll
+    for (int e = 10; e < 14; ++e)
+      o.nb[e] = fslot(F.TB, S, po, b.i + F.off[e][0], b.j + F.off[e][1], b.k + F.off[e][2]);
+  } else {
+    o.cB = -1;
+#pragma unroll
+    for (int e = 10; e < 14; ++e) o.nb[e] = -1;
+  }
+}
+
+__device__ __forceinline__ void load_po(int* po_s, const int* po, int N) {
+  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) po_s[p] = po[p];
+  __syncthreads();
+}
+
+// mode: kModeApply / kModeResid (vol_kernels.cuh values 0 / 1)
+__global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
+                             const uint32_t* __restrict__ fst, const int* __restrict__ po,
+                             const double* __restrict__ val, const double* __restrict__ u,
+                             const double* __restrict__ f, double* __restrict__ out, int mode) {
+  __shared__ int po_s[260];
+  load_po(po_s, po, N);
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_frows) return;
+  const int64_t fc = r / nfi;
+  const uint32_t st = fst[r - fc * nfi];
+  const FaceLP& F = flp[fc];
+  FaceRowSlots o;
+  face_row_slots(F, N, S, po_s, st & 0xffff, st >> 16, o);
+  double acc = val[r] * u[o.cA];
+#pragma unroll
+  for (int e = 0; e < 14; ++e)
+    if (o.nb[e] >= 0) acc = fma(val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
+  const double res = mode == 1 ? f[o.cA] - acc : acc;
+  out[o.cA] = res;
+  if (o.cB >= 0) out[o.cB] = res;
+}
+
+// GS colour step on face nodes of colour `colour`: compute into tmp, then write.
+__global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, const FaceLP* __restrict__ flp,
+                          const uint32_t* __restrict__ fst, const int* __restrict__ po, int64_t n_frows,
+                          const double* __restrict__ val, const double* __restrict__ u,
+                          const double* __restrict__ f, double* __restrict__ tmp) {
+  __shared__ int po_s[260];
+  load_po(po_s, po, N);
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t per_face = nfc;
+  const int64_t fc = x / per_face;
+  if (x >= per_face * (n_frows / nfi)) return;
+  const int64_t q = q0 + (x - fc * per_face);
+  const int64_t r = fc * nfi + q;
+  const uint32_t st = fst[q];
+  const FaceLP& F = flp[fc];
+  FaceRowSlots o;
+  face_row_slots(F, N, S, po_s, st & 0xffff, st >> 16, o);
+  double acc = f[o.cA];
+#pragma unroll
+  for (int e = 0; e < 14; ++e)
+    if (o.nb[e] >= 0) acc = fma(-val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
+  tmp[r] = acc / val[r];
+}
+
+__global__ void k_face_write(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, const FaceLP* __restrict__ flp,
+                             const uint32_t* __restrict__ fst, const int* __restrict__ po, int64_t n_faces,
+                             const double* __restrict__ tmp, double* __restrict__ u) {
+  __shared__ int po_s[260];
+  load_po(po_s, po, N);
+  const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t fc = x / nfc;
+  if (fc >= n_faces) return;
+  const int64_t q = q0 + (x - fc * nfc);
+  const uint32_t st = fst[q];
+  const FaceLP& F = flp[fc];
+  const int s = st & 0xffff, t = st >> 16;
+  const FaceNode a = face_node(F.lA, N, s, t);
+  const double v = tmp[fc * nfi + q];
+  u[fslot(F.TA, S, po_s, a.i, a.j, a.k)] = v;
+  if (F.TB >= 0) {
+    const FaceNode b = face_node(F.lB, N, s, t);
+    u[fslot(F.TB, S, po_s, b.i, b.j, b.k)] = v;
+  }
+}
+
+// dir 0: gather (local -> global), 1: scatter (global -> both copies), 2: sync (A -> B)
+__global__ void k_face_gather(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
+                              const uint32_t* __restrict__ fst, const int* __restrict__ fcidx,
+                              const int* __restrict__ po, int64_t base_f, double* __restrict__ local,
+                              double* __restrict__ glob, int dir) {
+  __shared__ int po_s[260];
+  load_po(po_s, po, N);
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_frows) return;
+  const int64_t fc = r / nfi;
+  const int64_t q = r - fc * nfi;
+  const uint32_t st = fst[q];
+  const FaceLP& F = flp[fc];
+  const int s = st & 0xffff, t = st >> 16;
+  const FaceNode a = face_node(F.lA, N, s, t);
+  const int64_t sA = fslot(F.TA, S, po_s, a.i, a.j, a.k);
+  int64_t sB = -1;
+  if (F.TB >= 0) {
+    const FaceNode b = face_node(F.lB, N, s, t);
+    sB = fslot(F.TB, S, po_s, b.i, b.j, b.k);
+  }
+  const int64_t g = base_f + F.fid * nfi + fcidx[q];
+  if (dir == 0) {
+    glob[g] = local[sA];
+  } else {
+    const double v = dir == 1 ? glob[g] : local[sA];
+    local[sA] = v;
+    if (sB >= 0) local[sB] = v;
+  }
+}
+
+__global__ void k_face_dot(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
+                           const uint32_t* __restrict__ fst, const int* __restrict__ po,
+                           const double* __restrict__ av, const double* __restrict__ bv, double* __restrict__ part) {
+  __shared__ int po_s[260];
+  __shared__ double red[32];
+  load_po(po_s, po, N);
+  double acc = 0.0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_frows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t fc = r / nfi;
+    const uint32_t st = fst[r - fc * nfi];
+    const FaceLP& F = flp[fc];
+    const FaceNode a = face_node(F.lA, N, st & 0xffff, st >> 16);
+    const int64_t sl = fslot(F.TA, S, po_s, a.i, a.j, a.k);
+    acc += av[sl] * bv[sl];
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    acc = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  }
+}
+
+static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+hhg_status face_apply(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* out) {
+  if (lv.n_frows == 0) return HHG_OK;
+  const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_fval_cons : lv.d_fval;
+  ProfScope ps(c, 2);
+  k_face_apply<<<nblk(lv.n_frows, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, lv.n_frows, lv.d_flp,
+                                                             lv.d_fst, lv.d_po, val, u, f, out, mode);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+hhg_status face_gs_step(Ctx* c, Level& lv, int op, int colour, double* u, const double* f) {
+  const int64_t nfc = lv.fcol[colour + 1] - lv.fcol[colour];
+  if (lv.n_frows == 0 || nfc == 0) return HHG_OK;
+  const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_fval_cons : lv.d_fval;
+  const int64_t n = nfc * lv.n_flp;
+  ProfScope ps(c, 2);
+  k_face_gs<<<nblk(n, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, nfc, lv.fcol[colour], lv.d_flp, lv.d_fst,
+                                                 lv.d_po, lv.n_frows, val, u, f, lv.d_ftmp);
+  HHG_LAUNCHED(c);
+  k_face_write<<<nblk(n, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, nfc, lv.fcol[colour], lv.d_flp,
+                                                    lv.d_fst, lv.d_po, lv.n_flp, lv.d_ftmp, u);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+hhg_status face_gather(Ctx* c, Level& lv, const double* local, double* glob, int dir) {
+  if (lv.n_frows == 0) return HHG_OK;
+  k_face_gather<<<nblk(lv.n_frows, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, lv.n_frows, lv.d_flp,
+                                                              lv.d_fst, lv.d_fcidx, lv.d_po, lv.gi.base_f,
+                                                              (double*)local, glob, dir);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+hhg_status face_sync(Ctx* c, Level& lv, double* u) { return face_gather(c, lv, u, nullptr, 2); }
+
+hhg_status face_dot(Ctx* c, Level& lv, const double* a, const double* b, double* part, int nblocks) {
+  if (lv.n_frows == 0) {
+    HHG_CK(c, cudaMemsetAsync(part, 0, nblocks * sizeof(double), c->stream));
+    return HHG_OK;
+  }
+  k_face_dot<<<nblocks, 256, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, lv.n_frows, lv.d_flp, lv.d_fst, lv.d_po, a, b,
+                                            part);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+// v at every copy of a shared face node <- sum of its copies (restriction partials)
+__global__ void k_face_sumcopies(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
+                                 const uint32_t* __restrict__ fst, const int* __restrict__ po,
+                                 double* __restrict__ v) {
+  __shared__ int po_s[260];
+  load_po(po_s, po, N);
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_frows) return;
+  const int64_t fc = r / nfi;
+  const uint32_t st = fst[r - fc * nfi];
+  const FaceLP& F = flp[fc];
+  if (F.TB < 0) return;
+  const int s = st & 0xffff, t = st >> 16;
+  const FaceNode a = face_node(F.lA, N, s, t), b = face_node(F.lB, N, s, t);
+  const int64_t sA = fslot(F.TA, S, po_s, a.i, a.j, a.k), sB = fslot(F.TB, S, po_s, b.i, b.j, b.k);
+  const double x = v[sA] + v[sB];
+  v[sA] = x;
+  v[sB] = x;
+}
+
+hhg_status face_sum_copies(Ctx* c, Level& lv, double* v) {
+  if (lv.n_frows == 0) return HHG_OK;
+  k_face_sumcopies<<<nblk(lv.n_frows, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, lv.n_frows, lv.d_flp,
+                                                                  lv.d_fst, lv.d_po, v);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+}  // namespace hhg

@@ -110,6 +110,17 @@ struct Band {
 constexpr int kMarchThreads = 256;
 constexpr int kRing = 16;  // plane slots (power of 2); >= 11 planes in flight ahead of use
 
+// Structured lower-primitive rows of one non-Dirichlet macro face (faces.cu).
+// Row entries: 0 centre; 1..6 in-face (ds,dt) = (1,0)(-1,0)(0,1)(0,-1)(-1,1)(1,-1);
+// 7..10 into macro A; 11..14 into macro B (zero if the face has no B).
+struct FaceLP {
+  int TA, TB;           // local macros (TA < TB; TB = -1 for a boundary face)
+  int8_t lA[3], lB[3];  // local vertex of the face's sorted vertices a<b<c in A / B
+  int8_t off[14][3];    // ijk offsets: [0..5] in-face (A frame), [6..9] into A, [10..13] into B (B frame)
+  int8_t mapA[15], mapB[15];  // partial-stencil direction -> entry (-1: not a neighbour)
+  int64_t fid;          // canonical face id
+};
+
 // ---------------------------------------------------------------------------
 // Per-level state
 // ---------------------------------------------------------------------------
@@ -146,6 +157,20 @@ struct Level {
   std::vector<Band> bands;
   Band* d_bands = nullptr;
   int slot_len = 0;
+  // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order
+  int64_t n_flp = 0, n_frows = 0;
+  int fcol[4] = {0, 0, 0, 0};      // colour offsets of q ((s+2t) mod 3 = 0,1,2)
+  FaceLP* d_flp = nullptr;
+  uint32_t* d_fst = nullptr;       // [nfi] s | t << 16 for q
+  int* d_fcidx = nullptr;          // [nfi] canonical in-face index of q
+  double* d_fval = nullptr;        // [15][n_frows] exact FEM, blended
+  double* d_fval_cons = nullptr;   // [15][n_frows] exact FEM, affine
+  double* d_ftmp = nullptr;        // [n_frows] GS scratch
+  int* d_po = nullptr;             // [N+2] plane offsets
+  // persistent GS work queue (k_gs_items)
+  int* d_gs_flags = nullptr;   // [nt_local][n_bands][4] sweep epoch of completed colour passes
+  int* d_gs_counter = nullptr; // [1]
+  int gs_epoch = 0;
 };
 
 struct Ctx {
@@ -172,6 +197,13 @@ struct Ctx {
   double* d_red = nullptr;            // reduction scratch
   double* h_red = nullptr;            // pinned
   int64_t red_n = 0;
+  // multigrid (vcycle.cu)
+  std::vector<uint16_t> own;          // [nt_local] owned faces (bits 0-3), edges (4-9), vertices (10-13)
+  uint16_t* d_own = nullptr;
+  std::vector<double*> vc_u, vc_f, vc_r;  // per-level work vectors
+  double* d_cg = nullptr;             // CG work: r p Ap at the coarse level (3 vectors)
+  int64_t cg_n = 0;
+  double* d_scal = nullptr;           // device scalars
   // profiling (hhg_profile)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -224,6 +256,23 @@ hhg_status check_cuda(Ctx* c, cudaError_t e, const char* what);
 // exponent table for the surrogate basis (index units): for q, m_q entries
 int n_coeffs(int q);
 void exponents(int q, std::vector<int>& l, std::vector<int>& m, std::vector<int>& n);
+
+// Structured face rows (faces.cu)
+hhg_status build_face_values(Ctx* c, Level& lv);
+hhg_status face_apply(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* out);
+hhg_status face_gs_step(Ctx* c, Level& lv, int op, int colour, double* u, const double* f);
+hhg_status face_gather(Ctx* c, Level& lv, const double* local, double* glob, int dir);
+hhg_status face_sync(Ctx* c, Level& lv, double* u);
+hhg_status face_dot(Ctx* c, Level& lv, const double* a, const double* b, double* part, int nblocks);
+hhg_status face_sum_copies(Ctx* c, Level& lv, double* v);
+
+// Operator pieces shared by ops.cu and vcycle.cu
+hhg_status apply_dev(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* y);
+hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f);
+hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out);
+hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* d_out);
+hhg_status zero_dir_slots(Ctx* c, Level& lv, double* out);
+hhg_status lp_sum_copies(Ctx* c, Level& lv, double* v);
 
 // Device geometry helpers (fem.cu)
 hhg_status launch_fem_partial(Ctx* c, int L, const uint32_t* d_slots, int64_t n, bool blended,

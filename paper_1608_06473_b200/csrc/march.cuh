@@ -60,17 +60,38 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-// Issue the bulk copy of plane p's band range into ring slot p % kRing.
-__device__ __forceinline__ void issue_plane(const double* ub, int N, int p, const Band& b, double* ring,
+// Issue the bulk copy of plane p's band range into ring slot p % kRing
+// (po = plane offset table in shared memory).
+__device__ __forceinline__ void issue_plane(const double* ub, const int* po, int p, const Band& b, double* ring,
                                             int slot_len, uint64_t* bars) {
-  const int64_t g0 = plane_off(N, p) + b.c_lo;
-  const int64_t a0 = g0 & ~(int64_t)1;
-  const int64_t a1 = (g0 + b.ncols + 1) & ~(int64_t)1;
+  const int g0 = po[p] + b.c_lo;
+  const int a0 = g0 & ~1;
+  const int a1 = (g0 + b.ncols + 1) & ~1;
   const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
   const int s = p & (kRing - 1);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   mbar_expect_tx(&bars[s], bytes);
   tma_load_1d(ring + s * slot_len, ub + a0, bytes, &bars[s]);
+}
+
+// Warp 0 issues planes [from, to] in parallel, one lane per plane (to - from < 32).
+__device__ __forceinline__ void issue_planes(const double* ub, const int* po, int from, int to, const Band& b,
+                                             double* ring, int slot_len, uint64_t* bars) {
+  if (threadIdx.x < 32) {
+    const int p = from + (int)threadIdx.x;
+    if (p <= to) issue_plane(ub, po, p, b, ring, slot_len, bars);
+  }
+}
+
+// 1/x to ~1 ulp: hardware approximation + two Newton steps (R16:
+// the GS division differs from IEEE division by at most a few ulp).
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
 }
 
 // Shared-memory carve-up common to the march kernels.
@@ -173,9 +194,8 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   march_prologue(sm, b, N, coef10, T, OP);
 
   const int last_plane = b.kmax + 1;
-  int next_issue = kRing;  // thread 0 only
-  if (threadIdx.x == 0)
-    for (int p = 0; p < kRing && p <= last_plane; ++p) issue_plane(ub, N, p, b, sm.ring, slot_len, sm.bars);
+  int next_issue = min(kRing, last_plane + 1);  // uniform across the CTA
+  issue_planes(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
 
   const int clo = b.c_lo;
   auto sptr = [&](int p, int pof) -> const double* {
@@ -225,9 +245,9 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
     // Warps drift freely between these barriers (ring of 16 keeps >= 8 planes ahead).
     if ((k & 7) == 0) {
       __syncthreads();
-      if (threadIdx.x == 0)
-        for (; next_issue <= k + kRing && next_issue <= last_plane; ++next_issue)
-          issue_plane(ub, N, next_issue, b, sm.ring, slot_len, sm.bars);
+      const int to = min(k + kRing, last_plane);
+      issue_planes(ub, sm.po, next_issue, to, b, sm.ring, slot_len, sm.bars);
+      next_issue = max(next_issue, to + 1);
     }
   }
 }
@@ -239,14 +259,10 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // visits its colour-c nodes k = delta + 4s (one per step of 4 planes).
 // ---------------------------------------------------------------------------
 template <int OP>
-__global__ void __launch_bounds__(kMarchThreads, 2)
-    k_gs_march(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
-               const double* __restrict__ coef10, const double* __restrict__ cons, int colour,
-               double* __restrict__ u, const double* __restrict__ f) {
-  extern __shared__ __align__(16) double smem[];
-  MarchSmem sm(smem, slot_len);
-  const int64_t T = blockIdx.x / n_bands;
-  const Band b = bands[blockIdx.x - T * n_bands];
+__device__ __forceinline__ void gs_band_pass(MarchSmem& sm, int slot_len, int N, int64_t S, const Band& b,
+                                             int64_t T, const double* __restrict__ coef10,
+                                             const double* __restrict__ cons, int colour,
+                                             double* __restrict__ u, const double* __restrict__ f) {
   double* ub = u + T * S;
   const Column q = make_column(b, N);
   double A[15], B[15];
@@ -256,9 +272,8 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
 
   const int last_plane = b.kmax + 1;
-  int next_issue = kRing;
-  if (threadIdx.x == 0)
-    for (int p = 0; p < kRing && p <= last_plane; ++p) issue_plane(ub, N, p, b, sm.ring, slot_len, sm.bars);
+  int next_issue = min(kRing, last_plane + 1);
+  issue_planes(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
   const int clo = b.c_lo;
   auto sptr = [&](int p) -> const double* {
     return sm.ring + (p & (kRing - 1)) * slot_len + ((sm.po[p] + clo) & 1);
@@ -267,12 +282,27 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   double* const wb = ub + q.c;
   int waited = -1;  // planes <= waited are resident
   const int nsteps = (b.kmax + 4) / 4;
+  // f of the next visited node is fetched one step ahead (hides HBM latency)
+  double f_next = 0.0;
+  {
+    const int k0 = delta;
+    if (q.active && k0 >= 1 && k0 <= q.len) f_next = __ldg(fb + sm.po[k0]);
+  }
   for (int s = 0; s < nsteps; ++s) {
     const int top = min(4 * s + 4, last_plane);
     for (int p = waited + 1; p <= top; ++p) mbar_wait(&sm.bars[p & (kRing - 1)], (p / kRing) & 1);
     waited = top;
     const int k = 4 * s + delta;
+    const double fv = f_next;
+    {
+      const int kn = k + 4;
+      if (q.active && kn >= 1 && kn <= q.len) f_next = __ldg(fb + sm.po[kn]);
+    }
     if (q.active && k >= 1 && k <= q.len) {
+      const double kd = (double)k;
+      // centre weight and its reciprocal first (off the critical path of the loads)
+      const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(sm.Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
+      const double rinv = rcp_nr(smc);
       const double* Pb = sptr(k - 1);
       const double* Pm = sptr(k);
       const double* Pt = sptr(k + 1);
@@ -280,32 +310,97 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
                              Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
       const int pk = sm.po[k];
-      const double fv = __ldg(fb + pk);
       double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      double smc;
       if (OP == HHG_OP_SURROGATE) {
-        const double kd = (double)k;
 #pragma unroll
         for (int w = 0; w < 15; ++w) {
+          if (w == kMC) continue;
           const double sw = fma(fma(sm.Cw[w], kd, B[w]), kd, A[w]);
-          if (w == kMC) smc = sw;
-          else acc[w % 5] = fma(sw, uu[w], acc[w % 5]);
+          acc[w % 5] = fma(sw, uu[w], acc[w % 5]);
         }
       } else {
 #pragma unroll
         for (int w = 0; w < 15; ++w) {
-          if (w == kMC) smc = A[w];
-          else acc[w % 5] = fma(A[w], uu[w], acc[w % 5]);
+          if (w == kMC) continue;
+          acc[w % 5] = fma(A[w], uu[w], acc[w % 5]);
         }
       }
       const double r = (acc[0] + acc[1]) + (acc[2] + acc[3]) + acc[4];
-      wb[pk] = (fv - r) / smc;
+      wb[pk] = (fv - r) * rinv;
     }
-    // all warps done with planes <= 4s+2 (next step reads >= 4s+3)
+    // every 3 steps: all warps done with planes <= 4s+2 (next step reads >= 4s+3);
+    // refill up to plane 4s+18 (the following 3 steps need <= 4s+16).
+    if (s % 3 == 2 || s == nsteps - 1) {
+      __syncthreads();
+      const int to = min(4 * s + 2 + kRing, last_plane);
+      issue_planes(ub, sm.po, next_issue, to, b, sm.ring, slot_len, sm.bars);
+      next_issue = max(next_issue, to + 1);
+    }
+  }
+}
+
+// One colour pass, one CTA per (macro, band).
+template <int OP>
+__global__ void __launch_bounds__(kMarchThreads, 2)
+    k_gs_march(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
+               const double* __restrict__ coef10, const double* __restrict__ cons, int colour,
+               double* __restrict__ u, const double* __restrict__ f) {
+  extern __shared__ __align__(16) double smem[];
+  MarchSmem sm(smem, slot_len);
+  const int64_t T = blockIdx.x / n_bands;
+  const Band b = bands[blockIdx.x - T * n_bands];
+  gs_band_pass<OP>(sm, slot_len, N, S, b, T, coef10, cons, colour, u, f);
+}
+
+// ---------------------------------------------------------------------------
+// Whole volume GS (4 colours) as ONE persistent launch.  Work item =
+// (macro, band, colour) colour pass; items are handed out in the order
+// (macro group of G, colour, macro, band) by an atomic counter, and item
+// (m,b,c) starts once items (m,b',c-1), |b'-b| <= 1, have completed
+// (completion flags = sweep epoch).  That is exactly the colour order of the
+// 4-colour GS: colour c of band b reads only bands b-1..b+1, and colour-c nodes
+// are never neighbours of each other.  A group's u and f stay L2-resident
+// across its four colours, so HBM sees ~1x u, f, u instead of 4x.  Items only
+// wait on items handed out earlier (to running CTAs) => deadlock-free.
+// ---------------------------------------------------------------------------
+template <int OP>
+__global__ void __launch_bounds__(kMarchThreads, 2)
+    k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
+               const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
+               const double* __restrict__ f, int64_t ntl, int G, int* __restrict__ counter,
+               int* __restrict__ flags, int epoch) {
+  extern __shared__ __align__(16) double smem[];
+  MarchSmem sm(smem, slot_len);
+  __shared__ int s_item;
+  const int64_t per_group = (int64_t)G * n_bands * 4;
+  const int64_t total = ntl * n_bands * 4;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
-    if (threadIdx.x == 0)
-      for (; next_issue <= 4 * s + 2 + kRing && next_issue <= last_plane; ++next_issue)
-        issue_plane(ub, N, next_issue, b, sm.ring, slot_len, sm.bars);
+    const int64_t item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const int64_t g = item / per_group;
+    const int64_t r = item - g * per_group;
+    const int64_t Gg = min((int64_t)G, ntl - g * G);  // macros in this group
+    const int colour = (int)(r / (Gg * n_bands));
+    const int64_t rr = r - (int64_t)colour * Gg * n_bands;
+    const int64_t T = g * G + rr / n_bands;
+    const int band = (int)(rr % n_bands);
+    if (threadIdx.x == 0 && colour > 0) {
+      for (int bb = max(0, band - 1); bb <= min(n_bands - 1, band + 1); ++bb) {
+        const volatile int* fl = flags + ((T * n_bands + bb) * 4 + colour - 1);
+        while (*fl != epoch) __nanosleep(64);
+      }
+      __threadfence();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+    const Band b = bands[band];
+    gs_band_pass<OP>(sm, slot_len, N, S, b, T, coef10, cons, colour, u, f);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
   }
 }
 

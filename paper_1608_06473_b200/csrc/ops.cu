@@ -108,9 +108,11 @@ __device__ inline double block_sum(double v) {
   return v;
 }
 
-__global__ void k_sumsq(int N, int64_t S, int64_t P, int64_t ntl, const double* __restrict__ r,
-                        int64_t n_rows, const uint32_t* __restrict__ lp_owner_col,
-                        const uint64_t* __restrict__ rp, double* __restrict__ part) {
+// sum over unique unknowns of a*b: volume interiors + CSR rows at their owner
+// copy (face rows: faces.cu::k_face_dot)
+__global__ void k_dot(int N, int64_t S, int64_t P, int64_t ntl, const double* __restrict__ a,
+                      const double* __restrict__ b, int64_t n_rows, const uint32_t* __restrict__ lp_owner_col,
+                      const uint64_t* __restrict__ rp, double* __restrict__ part) {
   double acc = 0.0;
   const int64_t tot = ntl * P;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
@@ -119,16 +121,25 @@ __global__ void k_sumsq(int N, int64_t S, int64_t P, int64_t ntl, const double* 
     int i, j, k;
     decode_pos(N, p, i, j, k);
     if (i < 1 || j < 1 || k < 1 || i + j + k > N - 1) continue;
-    double v = r[T * S + p];
-    acc += v * v;
+    acc += a[T * S + p] * b[T * S + p];
   }
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_rows;
        q += (int64_t)gridDim.x * blockDim.x) {
-    double v = r[lp_owner_col[rp[q]]];
-    acc += v * v;
+    const uint32_t s = lp_owner_col[rp[q]];
+    acc += a[s] * b[s];
   }
   acc = block_sum(acc);
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+// CSR rows: every copy <- sum of all copies (ascending macro order)
+__global__ void k_lp_sumcopies(int64_t n_rows, const uint64_t* __restrict__ cp, const uint32_t* __restrict__ copy,
+                               double* __restrict__ v) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_rows) return;
+  double s = 0.0;
+  for (uint64_t c = cp[r]; c < cp[r + 1]; ++c) s += v[copy[c]];
+  for (uint64_t c = cp[r]; c < cp[r + 1]; ++c) v[copy[c]] = s;
 }
 
 __global__ void k_final_sum(const double* __restrict__ part, int n, double* __restrict__ out) {
@@ -253,6 +264,41 @@ static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, cons
   return HHG_OK;
 }
 
+template <int OP>
+static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f) {
+  const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
+  static int grid = 0;
+  if (grid == 0) {
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    int dev = 0, sms = 0, per_sm = 0;
+    HHG_CK(c, cudaGetDevice(&dev));
+    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP>, kMarchThreads,
+                                                            march_smem_bytes(520, 256)));
+    grid = sms * std::max(per_sm, 1);
+  }
+  const int nb = (int)lv.bands.size();
+  // macro group: u and f of G macros (~90 MB) stay L2-resident across the 4
+  // colours, and a colour stage (G x bands items) is several CTA waves long so
+  // that stage c+1 rarely waits for stage c.
+  const double per_macro = 2.0 * (double)lv.S * sizeof(double);
+  static double l2_target = -1.0;
+  if (l2_target < 0) {
+    const char* e = getenv("HHG_GS_GROUP_MB");
+    l2_target = e ? atof(e) * 1e6 : 90.0e6;
+  }
+  int G = (int)std::max(1.0, std::min((double)c->nt_local, l2_target / per_macro));
+  lv.gs_epoch += 1;
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
+  const int64_t items = c->nt_local * nb * 4;
+  ProfScope ps(c, 1);
+  k_gs_items<OP><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G,
+      lv.d_gs_counter, lv.d_gs_flags, lv.gs_epoch);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
                               const double* f, double* out) {
   if (mode == kModeGS && !force_v1() && !lv.bands.empty()) {
@@ -279,6 +325,8 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
 
 static hhg_status lp_pass(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f,
                           double* out) {
+  hhg_status stf = face_apply(c, lv, op, mode, u, f, out);
+  if (stf != HHG_OK) return stf;
   if (lv.n_rows == 0) return HHG_OK;
   const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_val_cons : lv.d_val;
   ProfScope ps(c, 2);
@@ -296,18 +344,45 @@ static hhg_status zero_dir(Ctx* c, Level& lv, double* out) {
   return HHG_OK;
 }
 
-hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out) {
-  if (c->red_n < kRedBlocks + 1) {
-    HHG_CK(c, cudaMalloc(&c->d_red, (kRedBlocks + 1) * sizeof(double)));
+hhg_status zero_dir_slots(Ctx* c, Level& lv, double* out) { return zero_dir(c, lv, out); }
+
+// a.b over the unique unknowns into the device scalar d_out (fixed grids: deterministic)
+static hhg_status ensure_red(Ctx* c) {
+  if (c->red_n < 2 * kRedBlocks + 1) {
+    HHG_CK(c, cudaMalloc(&c->d_red, (2 * kRedBlocks + 1) * sizeof(double)));
     HHG_CK(c, cudaMallocHost(&c->h_red, 2 * sizeof(double)));
-    c->red_n = kRedBlocks + 1;
+    c->red_n = 2 * kRedBlocks + 1;
   }
-  k_sumsq<<<kRedBlocks, 256, 0, c->stream>>>(lv.N, lv.S, lv.P, c->nt_local, r, lv.n_rows, lv.d_col,
-                                             lv.d_row_ptr, c->d_red);
+  return HHG_OK;
+}
+
+hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* d_out) {
+  hhg_status st0 = ensure_red(c);
+  if (st0 != HHG_OK) return st0;
+  ProfScope ps(c, 3);
+  k_dot<<<kRedBlocks, 256, 0, c->stream>>>(lv.N, lv.S, lv.P, c->nt_local, a, b, lv.n_rows, lv.d_col,
+                                           lv.d_row_ptr, c->d_red);
   HHG_LAUNCHED(c);
-  k_final_sum<<<1, 1024, 0, c->stream>>>(c->d_red, kRedBlocks, c->d_red + kRedBlocks);
+  hhg_status stf = face_dot(c, lv, a, b, c->d_red + kRedBlocks, kRedBlocks);
+  if (stf != HHG_OK) return stf;
+  k_final_sum<<<1, 1024, 0, c->stream>>>(c->d_red, 2 * kRedBlocks, d_out);
   HHG_LAUNCHED(c);
-  HHG_CK(c, cudaMemcpyAsync(c->h_red, c->d_red + kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  return HHG_OK;
+}
+
+hhg_status lp_sum_copies(Ctx* c, Level& lv, double* v) {
+  if (lv.n_rows) {
+    k_lp_sumcopies<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy, v);
+    HHG_LAUNCHED(c);
+  }
+  return face_sum_copies(c, lv, v);
+}
+
+hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out) {
+  hhg_status st = ensure_red(c);
+  if (st != HHG_OK) return st;
+  if ((st = dot_dev(c, lv, r, r, c->d_red + 2 * kRedBlocks)) != HHG_OK) return st;
+  HHG_CK(c, cudaMemcpyAsync(c->h_red, c->d_red + 2 * kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   HHG_CK(c, cudaStreamSynchronize(c->stream));
   *out = std::sqrt(c->h_red[0]);
   return HHG_OK;
@@ -316,6 +391,10 @@ hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out) {
 hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
   const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_val_cons : lv.d_val;
   for (int s = 0; s < kNumLpSteps; ++s) {
+    if (s >= kStepFace0) {  // face colours: structured face rows
+      hhg_status stf = face_gs_step(c, lv, op, s - kStepFace0, u, f);
+      if (stf != HHG_OK) return stf;
+    }
     int64_t r0 = lv.step_start[s], r1 = lv.step_start[s + 1];
     if (r1 <= r0) continue;
     ProfScope ps(c, 2);
@@ -324,6 +403,17 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
     HHG_LAUNCHED(c);
     k_lp_write<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_copy_ptr, lv.d_copy, lv.d_tmp, u);
     HHG_LAUNCHED(c);
+  }
+  static int mode = -1;  // HHG_GS_KERNEL=passes -> 4 colour launches
+  if (mode < 0) {
+    const char* e = getenv("HHG_GS_KERNEL");
+    mode = (e && std::string(e) == "passes") ? 1 : 0;
+  }
+  const bool march_ok = !force_v1() && !lv.bands.empty() &&
+                        ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
+  if (march_ok && mode == 0) {
+    return op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
+                                  : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
   }
   for (int col = 0; col < 4; ++col) {
     hhg_status st = volume_pass(c, lv, op, kModeGS, col, u, f, u);
@@ -407,6 +497,7 @@ extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local,
                                                             lv.d_row_gid, sl.dev, dglob, 0);
     HHG_LAUNCHED(c);
   }
+  if ((st = face_gather(c, lv, sl.dev, dglob, 0)) != HHG_OK) return st;
   if (host_glob) {
     HHG_CK(c, cudaMemcpyAsync(glob, dglob, lv.gi.n_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     HHG_CK(c, cudaStreamSynchronize(c->stream));
@@ -439,6 +530,7 @@ extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob,
                                                             lv.d_row_gid, sl.dev, (double*)dglob, 1);
     HHG_LAUNCHED(c);
   }
+  if ((st = face_gather(c, lv, sl.dev, (double*)dglob, 1)) != HHG_OK) return st;
   if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
   if ((st = unstage(c, sl, lv.n_local)) != HHG_OK) return st;
   if (tmp) {
@@ -459,6 +551,7 @@ extern "C" hhg_status hhg_sync_copies(hhg_ctx ctx, int L, double* local) {
     k_lp_sync<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy, sl.dev);
     HHG_LAUNCHED(c);
   }
+  if ((st = face_sync(c, lv, sl.dev)) != HHG_OK) return st;
   if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
   return unstage(c, sl, lv.n_local);
 }

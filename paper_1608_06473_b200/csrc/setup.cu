@@ -73,6 +73,91 @@ static int local_of(const int64_t* tv, int64_t g) {
   return -1;
 }
 
+// Structured rows of the non-Dirichlet faces (FaceLP, hhg_internal.h).
+static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
+  const int N = lv.N;
+  const int64_t nfi = lv.gi.nfi;
+  // in-face node order: colour-major ((s+2t) mod 3), then canonical (t outer, s inner)
+  std::vector<uint32_t> fst;
+  std::vector<int> fcidx;
+  for (int col = 0; col < 3; ++col) {
+    lv.fcol[col] = (int)fst.size();
+    int ci = 0;
+    for (int t = 1; t <= N - 2; ++t)
+      for (int s = 1; s <= N - 1 - t; ++s, ++ci)
+        if ((s + 2 * t) % 3 == col) {
+          fst.push_back((uint32_t)s | ((uint32_t)t << 16));
+          fcidx.push_back(ci);
+        }
+  }
+  lv.fcol[3] = (int)fst.size();
+  const int D[6][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {-1, 1}, {1, -1}};
+  std::vector<FaceLP> flp;
+  for (int64_t f = 0; f < c->n_f; ++f) {
+    if (tp.fdir[f] || tp.finc[f].empty()) continue;
+    const int64_t key = tp.fkey[f];
+    const int64_t vc = key % c->nv, ab = key / c->nv;
+    const int64_t va = ab / c->nv, vb = ab % c->nv;
+    FaceLP F{};
+    F.fid = f;
+    F.TA = tp.finc[f][0];
+    F.TB = tp.finc[f].size() > 1 ? tp.finc[f][1] : -1;
+    for (int side = 0; side < 2; ++side) {
+      const int T = side == 0 ? F.TA : F.TB;
+      int8_t* l = side == 0 ? F.lA : F.lB;
+      int8_t* map = side == 0 ? F.mapA : F.mapB;
+      for (int w = 0; w < 15; ++w) map[w] = -1;
+      if (T < 0) continue;
+      const int64_t* gv = c->topo[T].gv;
+      l[0] = (int8_t)local_of(gv, va);
+      l[1] = (int8_t)local_of(gv, vb);
+      l[2] = (int8_t)local_of(gv, vc);
+      const int lf = 6 - l[0] - l[1] - l[2];
+      int n_into = 0;
+      for (int w = 0; w < 15; ++w) {
+        const int* dv = kDirHost[w];
+        const int dw[4] = {-dv[0] - dv[1] - dv[2], dv[0], dv[1], dv[2]};
+        if (w == kMC) { map[w] = 0; continue; }
+        if (dw[lf] == 0) {  // in-face: (ds, dt) = (dw[lb], dw[lc])
+          for (int e = 0; e < 6; ++e)
+            if (D[e][0] == dw[l[1]] && D[e][1] == dw[l[2]]) {
+              map[w] = (int8_t)(1 + e);
+              if (side == 0) for (int x = 0; x < 3; ++x) F.off[e][x] = (int8_t)dv[x];
+            }
+        } else if (dw[lf] == 1) {
+          map[w] = (int8_t)((side == 0 ? 7 : 11) + n_into);
+          for (int x = 0; x < 3; ++x) F.off[(side == 0 ? 6 : 10) + n_into][x] = (int8_t)dv[x];
+          ++n_into;
+        }
+      }
+      if (n_into != 4) return set_err(c, HHG_ERR_MESH, "face with != 4 into-macro directions");
+    }
+    flp.push_back(F);
+  }
+  lv.n_flp = (int64_t)flp.size();
+  lv.n_frows = lv.n_flp * nfi;
+  std::vector<int> po(N + 2);
+  for (int p = 0; p <= N + 1; ++p) po[p] = (int)plane_off(N, p);
+  auto up = [&](auto*& dptr, const auto& vec) -> hhg_status {
+    using TT = typename std::remove_reference<decltype(vec)>::type::value_type;
+    size_t bytes = std::max<size_t>(vec.size(), 1) * sizeof(TT);
+    HHG_CK(c, cudaMalloc((void**)&dptr, bytes));
+    if (!vec.empty())
+      HHG_CK(c, cudaMemcpy(dptr, vec.data(), vec.size() * sizeof(TT), cudaMemcpyHostToDevice));
+    return HHG_OK;
+  };
+  hhg_status st;
+  if ((st = up(lv.d_flp, flp)) != HHG_OK) return st;
+  if ((st = up(lv.d_fst, fst)) != HHG_OK) return st;
+  if ((st = up(lv.d_fcidx, fcidx)) != HHG_OK) return st;
+  if ((st = up(lv.d_po, po)) != HHG_OK) return st;
+  const size_t nv = (size_t)std::max<int64_t>(lv.n_frows, 1);
+  HHG_CK(c, cudaMalloc(&lv.d_fval, 15 * nv * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&lv.d_fval_cons, 15 * nv * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&lv.d_ftmp, nv * sizeof(double)));
+  return build_face_values(c, lv);
+}
+
 // Build lower-primitive rows of one level.
 static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   Level& lv = c->levels[L];
@@ -134,13 +219,18 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
       for (int t = 1; t <= N - 2; ++t)
         for (int s = 1; s <= N - 1 - t; ++s) {
           if ((s + 2 * t) % 3 != col) continue;
-          (tp.fdir[f] ? drows : rows).push_back(RowDesc{2, s, t, f});
+          // non-Dirichlet face nodes are handled by the structured face rows below
+          if (tp.fdir[f]) drows.push_back(RowDesc{2, s, t, f});
         }
     steps[4 + col] = (int64_t)rows.size();
   }
   for (int s = 0; s <= kNumLpSteps; ++s) lv.step_start[s] = steps[s];
   lv.n_rows = (int64_t)rows.size();
-  lv.n_owned = lv.n_rows + c->nt_local * g.nvi;
+  {
+    hhg_status stf = build_face_rows(c, tp, lv);
+    if (stf != HHG_OK) return stf;
+  }
+  lv.n_owned = lv.n_rows + lv.n_frows + c->nt_local * g.nvi;
 
   const int64_t S = lv.S;
   auto is_dir = [&](int64_t gid) -> bool {
@@ -301,6 +391,12 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if ((st = up(lv.d_dir_slot, dslot)) != HHG_OK) return st;
   if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
   if ((st = up(lv.d_bands, lv.bands)) != HHG_OK) return st;
+  {
+    const size_t nfl = (size_t)c->nt_local * std::max<size_t>(lv.bands.size(), 1) * 4;
+    HHG_CK(c, cudaMalloc(&lv.d_gs_flags, nfl * sizeof(int)));
+    HHG_CK(c, cudaMemset(lv.d_gs_flags, 0, nfl * sizeof(int)));
+    HHG_CK(c, cudaMalloc(&lv.d_gs_counter, sizeof(int)));
+  }
   HHG_CK(c, cudaMalloc(&lv.d_val, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_val_cons, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_tmp, std::max<int64_t>(nr, 1) * sizeof(double)));
@@ -322,7 +418,8 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
 static void free_level(Level& lv) {
   void* ps[] = {lv.d_row_ptr, lv.d_col, lv.d_val, lv.d_val_cons, lv.d_copy_ptr, lv.d_copy,
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
-                lv.d_coef10, lv.d_bands};
+                lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
+                lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
@@ -453,6 +550,19 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
   }
   for (int64_t f = 0; f < c->n_f; ++f)
     if (tp.finc[f].size() > 2) return fail(HHG_ERR_MESH, "face shared by more than two tets");
+  // primitive ownership (lowest local macro id) for the restriction R = P^T
+  c->own.assign(c->nt_local, 0);
+  for (int64_t T = 0; T < c->nt_local; ++T) {
+    const MacroTopo& m = c->topo[T];
+    uint16_t o = 0;
+    for (int f = 0; f < 4; ++f)
+      if (tp.finc[m.f[f]][0] == T) o |= (uint16_t)(1u << f);
+    for (int e = 0; e < 6; ++e)
+      if (tp.einc[m.e[e]][0] == T) o |= (uint16_t)(1u << (4 + e));
+    for (int v = 0; v < 4; ++v)
+      if (tp.vinc[m.gv[v]][0] == T) o |= (uint16_t)(1u << (10 + v));
+    c->own[T] = o;
+  }
   // Dirichlet closure
   for (int64_t T = 0; T < c->nt_local; ++T) {
     const MacroTopo& m = c->topo[T];
@@ -526,6 +636,12 @@ extern "C" void hhg_destroy(hhg_ctx ctx) {
     if (p) cudaFree(p);
   if (c->d_red) cudaFree(c->d_red);
   if (c->h_red) cudaFreeHost(c->h_red);
+  for (auto* v : {&c->vc_u, &c->vc_f, &c->vc_r})
+    for (double* p : *v)
+      if (p) cudaFree(p);
+  if (c->d_cg) cudaFree(c->d_cg);
+  if (c->d_scal) cudaFree(c->d_scal);
+  if (c->d_own) cudaFree(c->d_own);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto& v : c->ev_rec)
     for (auto& p : v) {

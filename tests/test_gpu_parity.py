@@ -183,3 +183,24 @@ def test_errors_are_reported():
     with pytest.raises(hhg.HHGError) as e:
         hhg.Ctx.from_mesh(wrong_r, 3)
     assert e.value.status == 2
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_hierarchy(mesh_name, L):
+    return solvers.Hierarchy(MESHES[mesh_name](), L, 2, 2)
+
+
+@pytest.mark.parametrize("mesh_name,L,cycles", [("tet", 4, 3), ("shell60", 4, 3), ("shell120", 3, 2)])
+def test_vcycle_history_matches_oracle(mesh_name, L, cycles):
+    """V(3,3), coarse 50 CG at L=2, 4-colour GS on every level: residual
+    histories agree to 1e-10 relative (north_star), iterates to 1e-10."""
+    H = oracle_hierarchy(mesh_name, L)
+    num = H.num[L]
+    u0, f = vecs(num, (7, 8))
+    u_ref, hist_ref = H.solve(u0.copy(), f, cycles)
+    ctx = gpu_ctx(mesh_name, L)
+    du, df = to_local(ctx, L, u0), to_local(ctx, L, f)
+    hist = ctx.vcycle(L, du, df, n_cycles=cycles)
+    assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
+    assert rel(ctx.gather_global(L, du), u_ref) < 1e-10
+    assert hist[-1] < 0.1 * hist[0]
