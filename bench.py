@@ -248,15 +248,20 @@ def main():
     vg_ms, vg_n = prof["vol_gs"]
     roof = None
     if va_n:
-        dom = max(("vol_apply", va_ms, 16), ("vol_gs", vg_ms, 24), key=lambda t: t[1])
-        name, tot_ms, bpu = dom
-        per_launch_bytes = nvol * bpu if name == "vol_apply" else nvol * 24 / 4
-        n_launch = va_n if name == "vol_apply" else vg_n
-        # GS: 4 colour launches per sweep together move 24 B per unknown
-        achieved = per_launch_bytes / (tot_ms / n_launch * 1e-3) / 1e9
-        roof = {"kernel": name, "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
-                "bytes_per_unknown": bpu, "share_of_step": tot_ms / (ms * a.steps)}
+        # dominant volume kernel; algorithmic bytes per volume unknown:
+        # apply 16 B (u in, y out), GS sweep 24 B (u, f in; u out) -- one apply and
+        # one sweep per step, whatever the number of launches they take
+        dom = max(("vol_apply", va_ms, 16, va_n), ("vol_gs", vg_ms, 24, vg_n), key=lambda t: t[1])
+        name, tot_ms, bpu, n_launch = dom
+        achieved = nvol * bpu * a.steps / (tot_ms * 1e-3) / 1e9
+        roof = {"kernel": "k_gs_items (4-colour GS sweep)" if name == "vol_gs" else "k_vol_march (apply)",
+                "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
+                "bytes_per_unknown": bpu, "units_per_launch": nvol * a.steps // max(n_launch, 1),
+                "launches": n_launch, "avg_launch_ms": tot_ms / max(n_launch, 1),
+                "share_of_step": tot_ms / (ms * a.steps),
+                "apply_frac": nvol * 16 * a.steps / (va_ms * 1e-3) / 1e9 / hbm,
+                "gs_frac": (nvol * 24 * a.steps / (vg_ms * 1e-3) / 1e9 / hbm) if vg_n else None}
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -253,24 +253,24 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
-// GS colour pass: every node of colour c = (i+2j+3k) mod 4 of the band, in
-// place (eq. iteration-scheme).  Nodes of one colour are
-// never neighbours (R14), so the pass is order-free; each thread
-// visits its colour-c nodes k = delta + 4s (one per step of 4 planes).
+// GS colour pass over one band: every node of colour c = (i+2j+3k) mod 4 of the
+// band, in place (eq. iteration-scheme).  Nodes of one
+// colour are never neighbours (R14), so the pass is order-free; each
+// thread visits its colour-c nodes k = delta + 4s (one per step of 4 planes).
+// The column coefficients (A, B) are computed by the caller once per band.
 // ---------------------------------------------------------------------------
 template <int OP>
-__device__ __forceinline__ void gs_band_pass(MarchSmem& sm, int slot_len, int N, int64_t S, const Band& b,
-                                             int64_t T, const double* __restrict__ coef10,
-                                             const double* __restrict__ cons, int colour,
-                                             double* __restrict__ u, const double* __restrict__ f) {
-  double* ub = u + T * S;
-  const Column q = make_column(b, N);
-  double A[15], B[15];
-  column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
-  march_prologue(sm, b, N, coef10, T, OP);
+__device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int N, const Band& b, const Column& q,
+                                               const double (&A)[15], const double (&B)[15], int colour,
+                                               double* __restrict__ ub, const double* __restrict__ fb,
+                                               double* __restrict__ wb) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kRing; ++s) mbar_init(&sm.bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
   // colour(i,j,k) = (d + j + 3k) mod 4 == colour  <=>  k == 3 (colour - d - j) mod 4
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
-
   const int last_plane = b.kmax + 1;
   int next_issue = min(kRing, last_plane + 1);
   issue_planes(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
@@ -278,29 +278,24 @@ __device__ __forceinline__ void gs_band_pass(MarchSmem& sm, int slot_len, int N,
   auto sptr = [&](int p) -> const double* {
     return sm.ring + (p & (kRing - 1)) * slot_len + ((sm.po[p] + clo) & 1);
   };
-  const double* const fb = f + T * S + q.c;
-  double* const wb = ub + q.c;
-  int waited = -1;  // planes <= waited are resident
+  auto wait_plane = [&](int p) {
+    if (p <= last_plane) mbar_wait(&sm.bars[p & (kRing - 1)], (p / kRing) & 1);
+  };
   const int nsteps = (b.kmax + 4) / 4;
-  // f of the next visited node is fetched one step ahead (hides HBM latency)
   double f_next = 0.0;
-  {
-    const int k0 = delta;
-    if (q.active && k0 >= 1 && k0 <= q.len) f_next = __ldg(fb + sm.po[k0]);
-  }
+  if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
+  wait_plane(0);
   for (int s = 0; s < nsteps; ++s) {
-    const int top = min(4 * s + 4, last_plane);
-    for (int p = waited + 1; p <= top; ++p) mbar_wait(&sm.bars[p & (kRing - 1)], (p / kRing) & 1);
-    waited = top;
+    // planes 4s+1 .. 4s+4 become needed at step s (4s-1, 4s were waited before)
+    wait_plane(4 * s + 1);
+    wait_plane(4 * s + 2);
+    wait_plane(4 * s + 3);
+    wait_plane(4 * s + 4);
     const int k = 4 * s + delta;
     const double fv = f_next;
-    {
-      const int kn = k + 4;
-      if (q.active && kn >= 1 && kn <= q.len) f_next = __ldg(fb + sm.po[kn]);
-    }
+    if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
     if (q.active && k >= 1 && k <= q.len) {
       const double kd = (double)k;
-      // centre weight and its reciprocal first (off the critical path of the loads)
       const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(sm.Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
       const double rinv = rcp_nr(smc);
       const double* Pb = sptr(k - 1);
@@ -309,7 +304,6 @@ __device__ __forceinline__ void gs_band_pass(MarchSmem& sm, int slot_len, int N,
       const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
                              Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
-      const int pk = sm.po[k];
       double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       if (OP == HHG_OP_SURROGATE) {
 #pragma unroll
@@ -326,7 +320,7 @@ __device__ __forceinline__ void gs_band_pass(MarchSmem& sm, int slot_len, int N,
         }
       }
       const double r = (acc[0] + acc[1]) + (acc[2] + acc[3]) + acc[4];
-      wb[pk] = (fv - r) * rinv;
+      wb[sm.po[k]] = (fv - r) * rinv;
     }
     // every 3 steps: all warps done with planes <= 4s+2 (next step reads >= 4s+3);
     // refill up to plane 4s+18 (the following 3 steps need <= 4s+16).
@@ -339,6 +333,17 @@ __device__ __forceinline__ void gs_band_pass(MarchSmem& sm, int slot_len, int N,
   }
 }
 
+template <int OP>
+__device__ __forceinline__ void band_setup(MarchSmem& sm, int N, const Band& b, int64_t T,
+                                           const double* __restrict__ coef10, const double* __restrict__ cons,
+                                           Column& q, double (&A)[15], double (&B)[15]) {
+  q = make_column(b, N);
+  column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
+  if (threadIdx.x < 15) sm.Cw[threadIdx.x] = (OP == HHG_OP_SURROGATE) ? coef10[T * 150 + threadIdx.x * 10 + 9] : 0.0;
+  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) sm.po[p] = (int)plane_off(N, p);
+  __syncthreads();
+}
+
 // One colour pass, one CTA per (macro, band).
 template <int OP>
 __global__ void __launch_bounds__(kMarchThreads, 2)
@@ -349,19 +354,24 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   MarchSmem sm(smem, slot_len);
   const int64_t T = blockIdx.x / n_bands;
   const Band b = bands[blockIdx.x - T * n_bands];
-  gs_band_pass<OP>(sm, slot_len, N, S, b, T, coef10, cons, colour, u, f);
+  Column q;
+  double A[15], B[15];
+  band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
+  gs_colour_pass<OP>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
 }
 
 // ---------------------------------------------------------------------------
-// Whole volume GS (4 colours) as ONE persistent launch.  Work item =
-// (macro, band, colour) colour pass; items are handed out in the order
-// (macro group of G, colour, macro, band) by an atomic counter, and item
-// (m,b,c) starts once items (m,b',c-1), |b'-b| <= 1, have completed
+// Whole volume GS (4 colours) as ONE persistent launch.  Work item = (macro,
+// band): the CTA runs the band's four colour passes in order; before colour c
+// it waits until bands b-1, b+1 of the same macro have finished colour c-1
 // (completion flags = sweep epoch).  That is exactly the colour order of the
 // 4-colour GS: colour c of band b reads only bands b-1..b+1, and colour-c nodes
-// are never neighbours of each other.  A group's u and f stay L2-resident
-// across its four colours, so HBM sees ~1x u, f, u instead of 4x.  Items only
-// wait on items handed out earlier (to running CTAs) => deadlock-free.
+// are never neighbours of each other.  Items are handed out in (macro, band)
+// order by an atomic counter, so the ~8 macros in flight keep u and f
+// L2-resident across their four colours (HBM sees ~1x u, f, u instead of 4x).
+// Only the single partially handed-out macro can wait on an item that is not
+// running yet; every other running item's neighbours run too => no deadlock
+// while the grid has more CTAs than a macro has bands.
 // ---------------------------------------------------------------------------
 template <int OP>
 __global__ void __launch_bounds__(kMarchThreads, 2)
@@ -372,35 +382,36 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   extern __shared__ __align__(16) double smem[];
   MarchSmem sm(smem, slot_len);
   __shared__ int s_item;
-  const int64_t per_group = (int64_t)G * n_bands * 4;
-  const int64_t total = ntl * n_bands * 4;
+  (void)G;
+  const int64_t total = ntl * n_bands;
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
     const int64_t item = s_item;
     __syncthreads();
     if (item >= total) break;
-    const int64_t g = item / per_group;
-    const int64_t r = item - g * per_group;
-    const int64_t Gg = min((int64_t)G, ntl - g * G);  // macros in this group
-    const int colour = (int)(r / (Gg * n_bands));
-    const int64_t rr = r - (int64_t)colour * Gg * n_bands;
-    const int64_t T = g * G + rr / n_bands;
-    const int band = (int)(rr % n_bands);
-    if (threadIdx.x == 0 && colour > 0) {
-      for (int bb = max(0, band - 1); bb <= min(n_bands - 1, band + 1); ++bb) {
-        const volatile int* fl = flags + ((T * n_bands + bb) * 4 + colour - 1);
-        while (*fl != epoch) __nanosleep(64);
-      }
-      __threadfence();
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    __syncthreads();
+    const int64_t T = item / n_bands;
+    const int band = (int)(item - T * n_bands);
     const Band b = bands[band];
-    gs_band_pass<OP>(sm, slot_len, N, S, b, T, coef10, cons, colour, u, f);
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
+    Column q;
+    double A[15], B[15];
+    band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
+    for (int colour = 0; colour < 4; ++colour) {
+      if (threadIdx.x == 0 && colour > 0) {
+        for (int bb = band - 1; bb <= band + 1; bb += 2) {
+          if (bb < 0 || bb >= n_bands) continue;
+          const volatile int* fl = flags + ((T * n_bands + bb) * 4 + colour - 1);
+          while (*fl != epoch) __nanosleep(32);
+        }
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+      __syncthreads();
+      gs_colour_pass<OP>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
+    }
   }
 }
 

@@ -290,7 +290,7 @@ static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f)
   int G = (int)std::max(1.0, std::min((double)c->nt_local, l2_target / per_macro));
   lv.gs_epoch += 1;
   HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
-  const int64_t items = c->nt_local * nb * 4;
+  const int64_t items = c->nt_local * nb;
   ProfScope ps(c, 1);
   k_gs_items<OP><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
       lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G,
