@@ -172,6 +172,26 @@ hhg_status hhg_sync_copies(hhg_ctx ctx, int L, double* local);
  * FEM stencils of the blended / affine geometry. */
 hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t macro, double* out);
 
+/* Multi-rank transport for contexts set up with nranks > 1 and
+ * nccl_unique_id == NULL (tests; production uses NCCL).  fn moves host buffers
+ * between all ranks: for every peer p, send_bytes[p] bytes (concatenated in
+ * rank order in send_buf) go to p, recv_bytes[p] bytes from p land in recv_buf;
+ * it returns 0 on success and must be called collectively.  Process-wide;
+ * applies to the following hhg_setup_macro_mesh calls.  host_only != 0 makes
+ * those setups build the partition and exchange plan on the host only (no
+ * CUDA calls; compute entry points then return HHG_ERR_STATE). */
+typedef int (*hhg_host_exchange_fn)(void* user, int nranks, const int64_t* send_bytes, const void* send_buf,
+                                    const int64_t* recv_bytes, void* recv_buf);
+hhg_status hhg_set_host_transport(hhg_host_exchange_fn fn, void* user, int host_only);
+
+/* Partition / exchange-plan diagnostics at level L: info[5] = {owned unknowns,
+ * values sent per sync, values received per sync, local macros, local + ghost
+ * macro blocks}.  hhg_plan_check runs the plan once on canonical node ids
+ * through the transport and returns the number of received ids that differ
+ * from the expected ones (0 = consistent).  Collective. */
+hhg_status hhg_plan_info(hhg_ctx ctx, int L, int64_t* info);
+hhg_status hhg_plan_check(hhg_ctx ctx, int L, int64_t* mismatches);
+
 /* Count of this library's kernel launches since setup (for the bench). */
 int64_t hhg_kernel_launches(hhg_ctx ctx);
 

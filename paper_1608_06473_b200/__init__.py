@@ -50,6 +50,12 @@ def lib():
     L.hhg_scatter_global.argtypes = [P, I32, P, P]
     L.hhg_sync_copies.argtypes = [P, I32, P]
     L.hhg_eval_stencils.argtypes = [P, I32, I32, I64, P]
+    L.hhg_set_host_transport.argtypes = [P, P, I32]
+    L.hhg_set_host_transport.restype = ctypes.c_int
+    L.hhg_plan_info.argtypes = [P, I32, ctypes.POINTER(I64)]
+    L.hhg_plan_info.restype = ctypes.c_int
+    L.hhg_plan_check.argtypes = [P, I32, ctypes.POINTER(I64)]
+    L.hhg_plan_check.restype = ctypes.c_int
     L.hhg_profile.argtypes = [P, I32]
     L.hhg_profile.restype = ctypes.c_int
     L.hhg_profile_read.argtypes = [P, I32, ctypes.POINTER(D), ctypes.POINTER(I64)]
@@ -85,6 +91,58 @@ def _ptr(x, n=None, writable=False):
     if n is not None and x.numel() < n:
         raise ValueError(f"vector too short: {x.numel()} < {n}")
     return x.data_ptr()
+
+
+HostExchangeFn = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
+                                  ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
+_keep_alive = []
+
+
+def set_torch_transport(host_only=False, group=None):
+    """Route the library's multi-rank exchanges through torch.distributed
+    point-to-point (any backend that moves CPU tensors, e.g. gloo) instead of
+    NCCL: plumbing for tests and CPU plan checks (hhg_set_host_transport)."""
+    import torch
+    import torch.distributed as dist
+
+    def cb(user, nranks, sb, send, rb, recv):
+        try:
+            me = dist.get_rank(group)
+            ts = sum(sb[p] for p in range(nranks))
+            tr = sum(rb[p] for p in range(nranks))
+            sbuf = torch.frombuffer((ctypes.c_char * max(ts, 1)).from_address(send), dtype=torch.uint8) if ts else None
+            rbuf = torch.frombuffer((ctypes.c_char * max(tr, 1)).from_address(recv), dtype=torch.uint8) if tr else None
+            reqs = []
+            so = ro = 0
+            for p in range(nranks):
+                if p == me:
+                    if sb[p]:
+                        rbuf[ro:ro + rb[p]].copy_(sbuf[so:so + sb[p]])
+                else:
+                    if sb[p]:
+                        reqs.append(dist.isend(sbuf[so:so + sb[p]].clone(), p, group=group))
+                    if rb[p]:
+                        reqs.append((dist.irecv(tmp := torch.empty(rb[p], dtype=torch.uint8), p, group=group),
+                                     tmp, ro, rb[p]))
+                so += sb[p]
+                ro += rb[p]
+            for r in reqs:
+                if isinstance(r, tuple):
+                    r[0].wait()
+                    rbuf[r[2]:r[2] + r[3]].copy_(r[1])
+                else:
+                    r.wait()
+            return 0
+        except Exception as e:  # pragma: no cover
+            import sys
+            sys.stderr.write(f"hhg host transport failed: {e}\n")
+            return 1
+
+    fn = HostExchangeFn(cb)
+    _keep_alive.append(fn)
+    st = lib().hhg_set_host_transport(ctypes.cast(fn, ctypes.c_void_p), None, 1 if host_only else 0)
+    if st != 0:
+        raise HHGError(st, "hhg_set_host_transport")
 
 
 class Ctx:
@@ -194,6 +252,16 @@ class Ctx:
         out = np.zeros((n_int, 15))
         self._check(self._lib.hhg_eval_stencils(self.h, L, OPS[op], macro, out.ctypes.data))
         return out
+
+    def plan_info(self, L):
+        info = (ctypes.c_int64 * 5)()
+        self._check(self._lib.hhg_plan_info(self.h, L, info))
+        return dict(zip(("owned", "send", "recv", "local_macros", "blocks"), list(info)))
+
+    def plan_check(self, L):
+        m = ctypes.c_int64()
+        self._check(self._lib.hhg_plan_check(self.h, L, ctypes.byref(m)))
+        return m.value
 
     @property
     def kernel_launches(self):

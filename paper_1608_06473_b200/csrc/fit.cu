@@ -114,6 +114,7 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
   Ctx* c = (Ctx*)ctx;
   if (!c) return HHG_ERR_INVALID;
   if (c->poisoned) return HHG_ERR_CUDA;
+  if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context");
   if (q < 0 || q > 4) return set_err(c, HHG_ERR_INVALID, "q must be in 0..4 (PAPER.md:530-534)");
   if (method != HHG_FIT_LSQP && method != HHG_FIT_IPOLY) return set_err(c, HHG_ERR_INVALID, "method");
   if (method == HHG_FIT_IPOLY && q != 2)

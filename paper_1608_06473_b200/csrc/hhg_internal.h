@@ -167,6 +167,18 @@ struct Level {
   double* d_fval_cons = nullptr;   // [15][n_frows] exact FEM, affine
   double* d_ftmp = nullptr;        // [n_frows] GS scratch
   int* d_po = nullptr;             // [N+2] plane offsets
+  std::vector<FaceLP> h_flp;       // host copies (exchange plan)
+  std::vector<uint32_t> h_fst;
+  std::vector<int> h_fcidx;
+  // exchange plan (dist.cu): values this rank receives from / sends to each peer
+  std::vector<int64_t> send_cnt, recv_cnt;   // [nranks] doubles per peer
+  std::vector<uint32_t> h_send_slot, h_recv_slot;
+  std::vector<int64_t> h_send_gid, h_recv_gid;  // canonical ids (plan checks)
+  uint32_t* d_send_slot = nullptr;
+  uint32_t* d_recv_slot = nullptr;
+  double* d_sendbuf = nullptr;
+  double* d_recvbuf = nullptr;
+  int64_t n_send = 0, n_recv = 0;
   // persistent GS work queue (k_gs_items)
   int* d_gs_flags = nullptr;   // [nt_local][n_bands][4] sweep epoch of completed colour passes
   int* d_gs_counter = nullptr; // [1]
@@ -179,7 +191,19 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   int rank = 0, nranks = 1;
   int L_max = 0;
-  int64_t nv = 0, nt = 0, nt_local = 0;
+  // nt_local macros owned by this rank are blocks [0, nt_local); ghost macros
+  // (owned elsewhere, sharing a vertex with a local macro) follow up to nt_blocks
+  int64_t nv = 0, nt = 0, nt_local = 0, nt_blocks = 0;
+  std::vector<int32_t> owner;         // [nt] rank of every global macro
+  std::vector<int64_t> g2b;           // [nt] global macro -> block (-1: absent)
+  // transport (dist.cu)
+  int transport = 0;                  // 0 none (1 rank), 1 NCCL, 2 host callback
+  void* nccl_comm = nullptr;          // ncclComm_t
+  void* host_fn = nullptr;            // hhg_host_exchange_fn
+  void* host_user = nullptr;
+  bool host_only = false;             // plan-only context (no CUDA), tests
+  double* h_stage = nullptr;          // pinned staging for the host transport
+  int64_t h_stage_n = 0;
   int64_t n_e = 0, n_f = 0;
   bool blended = true;
   std::vector<double> vertices, radius;
@@ -256,6 +280,17 @@ hhg_status check_cuda(Ctx* c, cudaError_t e, const char* what);
 // exponent table for the surrogate basis (index units): for q, m_q entries
 int n_coeffs(int q);
 void exponents(int q, std::vector<int>& l, std::vector<int>& m, std::vector<int>& n);
+
+// Distributed-memory support (dist.cu)
+hhg_status dist_init_transport(Ctx* c, const void* nccl_unique_id);
+void dist_destroy(Ctx* c);
+hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& send_bytes, const void* send,
+                               const std::vector<int64_t>& recv_bytes, void* recv, bool device);
+hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_slot,
+                           const std::vector<int64_t>& recv_gid, const std::vector<int32_t>& recv_rank,
+                           const std::vector<std::pair<int64_t, uint32_t>>& serve);
+hhg_status dist_sync(Ctx* c, Level& lv, double* v);
+hhg_status dist_allreduce_sum(Ctx* c, double* d_scalar);
 
 // Structured face rows (faces.cu)
 hhg_status build_face_values(Ctx* c, Level& lv);

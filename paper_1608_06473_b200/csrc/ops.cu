@@ -214,6 +214,7 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
   if (!c) return HHG_ERR_INVALID;
   if (c->poisoned) return HHG_ERR_CUDA;
+  if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context (hhg_set_host_transport host_only)");
   if (L < 2 || L > c->L_max) return set_err(c, HHG_ERR_INVALID, "L out of range");
   if (op < 0 || op > 2) return set_err(c, HHG_ERR_INVALID, "bad op");
   if (op == HHG_OP_SURROGATE && !c->levels[L].fitted)
@@ -367,7 +368,7 @@ hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* 
   if (stf != HHG_OK) return stf;
   k_final_sum<<<1, 1024, 0, c->stream>>>(c->d_red, 2 * kRedBlocks, d_out);
   HHG_LAUNCHED(c);
-  return HHG_OK;
+  return dist_allreduce_sum(c, d_out);
 }
 
 hhg_status lp_sum_copies(Ctx* c, Level& lv, double* v) {
@@ -396,13 +397,17 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
       if (stf != HHG_OK) return stf;
     }
     int64_t r0 = lv.step_start[s], r1 = lv.step_start[s + 1];
-    if (r1 <= r0) continue;
-    ProfScope ps(c, 2);
-    k_lp_gs_compute<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_row_ptr, lv.d_col, val, u, f,
-                                                               lv.d_tmp);
-    HHG_LAUNCHED(c);
-    k_lp_write<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_copy_ptr, lv.d_copy, lv.d_tmp, u);
-    HHG_LAUNCHED(c);
+    if (r1 > r0) {
+      ProfScope ps(c, 2);
+      k_lp_gs_compute<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_row_ptr, lv.d_col, val, u, f,
+                                                                 lv.d_tmp);
+      HHG_LAUNCHED(c);
+      k_lp_write<<<nblk(r1 - r0, 128), 128, 0, c->stream>>>(r0, r1, lv.d_copy_ptr, lv.d_copy, lv.d_tmp, u);
+      HHG_LAUNCHED(c);
+    }
+    // the next class step reads this step's values on every rank
+    hhg_status sts = dist_sync(c, lv, u);
+    if (sts != HHG_OK) return sts;
   }
   static int mode = -1;  // HHG_GS_KERNEL=passes -> 4 colour launches
   if (mode < 0) {
@@ -412,20 +417,23 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
   const bool march_ok = !force_v1() && !lv.bands.empty() &&
                         ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
   if (march_ok && mode == 0) {
-    return op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
-                                  : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
-  }
-  for (int col = 0; col < 4; ++col) {
-    hhg_status st = volume_pass(c, lv, op, kModeGS, col, u, f, u);
+    hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
+                                           : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
     if (st != HHG_OK) return st;
+  } else {
+    for (int col = 0; col < 4; ++col) {
+      hhg_status st = volume_pass(c, lv, op, kModeGS, col, u, f, u);
+      if (st != HHG_OK) return st;
+    }
   }
-  return HHG_OK;
+  return dist_sync(c, lv, u);  // ghost volume values for the other ranks
 }
 
 hhg_status apply_dev(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* y) {
   hhg_status st;
   if ((st = volume_pass(c, lv, op, mode, 0, u, f, y)) != HHG_OK) return st;
   if ((st = lp_pass(c, lv, op, mode, u, f, y)) != HHG_OK) return st;
+  if ((st = dist_sync(c, lv, y)) != HHG_OK) return st;  // owners' rows -> every copy / ghost
   return zero_dir(c, lv, y);
 }
 
@@ -479,7 +487,8 @@ extern "C" hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, con
 extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local, double* glob) {
   Ctx* c = (Ctx*)ctx;
   if (!c || L < 2 || L > c->L_max || !local || !glob) return HHG_ERR_INVALID;
-  if (c->nranks != 1) return set_err(c, HHG_ERR_INVALID, "gather_global: single-rank only");
+  if (c->host_only) return HHG_ERR_STATE;
+  // multi-rank: writes the entries this rank owns, 0 elsewhere (sum over ranks = global vector)
   Level& lv = c->levels[L];
   hhg_status st;
   Staged sl;
@@ -509,7 +518,9 @@ extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local,
 extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob, double* local) {
   Ctx* c = (Ctx*)ctx;
   if (!c || L < 2 || L > c->L_max || !local || !glob) return HHG_ERR_INVALID;
-  if (c->nranks != 1) return set_err(c, HHG_ERR_INVALID, "scatter_global: single-rank only");
+  if (c->host_only) return HHG_ERR_STATE;
+  // multi-rank: every rank passes the full global vector; owned rows fill their
+  // copies here and the sync fills the mirrors of nodes owned elsewhere
   Level& lv = c->levels[L];
   hhg_status st;
   Staged sl;
@@ -522,7 +533,7 @@ extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob,
     dglob = tmp;
   }
   HHG_CK(c, cudaMemsetAsync(sl.dev, 0, lv.n_local * sizeof(double), c->stream));
-  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
+  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_blocks);  // ghost interiors too
   k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, sl.dev, (double*)dglob, 1);
   HHG_LAUNCHED(c);
   if (lv.n_rows) {
@@ -531,6 +542,7 @@ extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob,
     HHG_LAUNCHED(c);
   }
   if ((st = face_gather(c, lv, sl.dev, (double*)dglob, 1)) != HHG_OK) return st;
+  if ((st = dist_sync(c, lv, sl.dev)) != HHG_OK) return st;
   if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
   if ((st = unstage(c, sl, lv.n_local)) != HHG_OK) return st;
   if (tmp) {
@@ -552,6 +564,7 @@ extern "C" hhg_status hhg_sync_copies(hhg_ctx ctx, int L, double* local) {
     HHG_LAUNCHED(c);
   }
   if ((st = face_sync(c, lv, sl.dev)) != HHG_OK) return st;
+  if ((st = dist_sync(c, lv, sl.dev)) != HHG_OK) return st;
   if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
   return unstage(c, sl, lv.n_local);
 }

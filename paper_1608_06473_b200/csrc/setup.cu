@@ -56,8 +56,9 @@ struct RowDesc {
 
 struct Topology {
   std::vector<int64_t> ekey, fkey;               // sorted unique keys
-  std::vector<std::vector<int32_t>> vinc, einc, finc;  // incident local macros
+  std::vector<std::vector<int32_t>> vinc, einc, finc;  // incident blocks (ascending global id)
   std::vector<uint8_t> vdir, edir, fdir;
+  std::vector<int32_t> vown, eown, fown;         // owner rank of each primitive
 };
 
 inline void corner(int lv, int N, int w[4]) {
@@ -94,7 +95,7 @@ static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
   const int D[6][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {-1, 1}, {1, -1}};
   std::vector<FaceLP> flp;
   for (int64_t f = 0; f < c->n_f; ++f) {
-    if (tp.fdir[f] || tp.finc[f].empty()) continue;
+    if (tp.fdir[f] || tp.finc[f].empty() || tp.fown[f] != c->rank) continue;
     const int64_t key = tp.fkey[f];
     const int64_t vc = key % c->nv, ab = key / c->nv;
     const int64_t va = ab / c->nv, vb = ab % c->nv;
@@ -136,6 +137,10 @@ static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
   }
   lv.n_flp = (int64_t)flp.size();
   lv.n_frows = lv.n_flp * nfi;
+  lv.h_flp = flp;
+  lv.h_fst = fst;
+  lv.h_fcidx = fcidx;
+  if (c->host_only) return HHG_OK;
   std::vector<int> po(N + 2);
   for (int p = 0; p <= N + 1; ++p) po[p] = (int)plane_off(N, p);
   auto up = [&](auto*& dptr, const auto& vec) -> hhg_status {
@@ -183,7 +188,7 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
     lv.bands.push_back(b);
     lv.slot_len = std::max(lv.slot_len, (b.ncols + 2 + 3) / 4 * 4);
   }
-  lv.n_local = lv.S * c->nt_local;
+  lv.n_local = lv.S * c->nt_blocks;
   GidInfo& g = lv.gi;
   g.N = N;
   g.nv = c->nv;
@@ -201,21 +206,28 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   std::vector<RowDesc> drows;  // Dirichlet lower nodes (all copies zeroed)
   int64_t steps[kNumLpSteps + 1];
   steps[0] = 0;
+  // rows: owned by this rank (owner of the lowest-id macro containing the node);
+  // Dirichlet nodes: every copy on this rank is zeroed
   for (int64_t v = 0; v < c->nv; ++v) {
     if (tp.vinc[v].empty()) continue;
-    (tp.vdir[v] ? drows : rows).push_back(RowDesc{0, 0, 0, v});
+    if (tp.vdir[v]) drows.push_back(RowDesc{0, 0, 0, v});
+    else if (tp.vown[v] == c->rank) rows.push_back(RowDesc{0, 0, 0, v});
   }
   steps[1] = (int64_t)rows.size();
   for (int col = 0; col < 2; ++col) {
-    for (int64_t e = 0; e < c->n_e; ++e)
+    for (int64_t e = 0; e < c->n_e; ++e) {
+      if (tp.einc[e].empty()) continue;
       for (int m = 1; m <= N - 1; ++m) {
         if ((m % 2) != col) continue;
-        (tp.edir[e] ? drows : rows).push_back(RowDesc{1, m, 0, e});
+        if (tp.edir[e]) drows.push_back(RowDesc{1, m, 0, e});
+        else if (tp.eown[e] == c->rank) rows.push_back(RowDesc{1, m, 0, e});
       }
+    }
     steps[2 + col] = (int64_t)rows.size();
   }
   for (int col = 0; col < 3; ++col) {
     for (int64_t f = 0; f < c->n_f; ++f)
+      if (!tp.finc[f].empty())
       for (int t = 1; t <= N - 2; ++t)
         for (int s = 1; s <= N - 1 - t; ++s) {
           if ((s + 2 * t) % 3 != col) continue;
@@ -373,6 +385,98 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   }
   lv.n_dir = (int64_t)dslot.size();
 
+  // ---- exchange plan (multi-rank): which slots of this rank mirror values
+  // owned elsewhere ((a) ghost-block slots read by the owned rows, (b) the
+  // local copies of lower-primitive nodes owned by another rank), and which
+  // owned values this rank serves.
+  if (c->nranks > 1) {
+    auto value_rank = [&](int64_t T, int i, int j, int k, int64_t& gid) -> int {
+      gid = node_gid(g, c->topo[T], i, j, k);
+      if (gid >= g.base_v) return c->owner[c->topo[T].gT];
+      if (gid < g.base_e) return tp.vown[gid];
+      if (gid < g.base_f) return tp.eown[(gid - g.base_e) / (N - 1)];
+      return tp.fown[(gid - g.base_f) / g.nfi];
+    };
+    std::vector<std::pair<uint32_t, int64_t>> cand;  // (slot, gid)
+    std::vector<int32_t> cand_rank;
+    auto consider = [&](int64_t T, int i, int j, int k) {
+      int64_t gid;
+      const int r = value_rank(T, i, j, k, gid);
+      if (r == c->rank || is_dir(gid)) return;
+      cand.push_back({(uint32_t)slot_of((int)T, i, j, k), gid});
+      cand_rank.push_back(r);
+    };
+    // (a) CSR columns in ghost blocks
+    for (int64_t e = 0; e < lv.nnz; ++e) {
+      const int64_t T = col[e] / S;
+      if (T < c->nt_local) continue;
+      int i, j, k;
+      decode_pos(N, col[e] - T * S, i, j, k);
+      consider(T, i, j, k);
+    }
+    // (a) face rows: the 4 into-B neighbours when B is a ghost
+    for (const FaceLP& F : lv.h_flp) {
+      if (F.TB < c->nt_local) continue;
+      for (int64_t q = 0; q < g.nfi; ++q) {
+        const int s = lv.h_fst[q] & 0xffff, t = lv.h_fst[q] >> 16;
+        int w[4] = {0, 0, 0, 0};
+        w[F.lB[0]] = N - s - t;
+        w[F.lB[1]] = s;
+        w[F.lB[2]] = t;
+        for (int e = 10; e < 14; ++e) consider(F.TB, w[1] + F.off[e][0], w[2] + F.off[e][1], w[3] + F.off[e][2]);
+      }
+    }
+    // (b) local copies of lower-primitive nodes owned elsewhere
+    {
+      std::vector<std::array<int, 4>> cps;
+      auto add_local = [&](const RowDesc& r) {
+        copies_of(r, cps);
+        for (auto& cpy : cps)
+          if (cpy[0] < c->nt_local) consider(cpy[0], cpy[1], cpy[2], cpy[3]);
+      };
+      for (int64_t v = 0; v < c->nv; ++v)
+        if (!tp.vinc[v].empty() && !tp.vdir[v] && tp.vown[v] != c->rank) add_local(RowDesc{0, 0, 0, v});
+      for (int64_t e = 0; e < c->n_e; ++e)
+        if (!tp.einc[e].empty() && !tp.edir[e] && tp.eown[e] != c->rank)
+          for (int m = 1; m <= N - 1; ++m) add_local(RowDesc{1, m, 0, e});
+      for (int64_t f = 0; f < c->n_f; ++f)
+        if (!tp.finc[f].empty() && !tp.fdir[f] && tp.fown[f] != c->rank)
+          for (int t = 1; t <= N - 2; ++t)
+            for (int s = 1; s <= N - 1 - t; ++s) add_local(RowDesc{2, s, t, f});
+    }
+    // dedupe by slot
+    std::vector<size_t> ord(cand.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](size_t a, size_t b) { return cand[a].first < cand[b].first; });
+    std::vector<uint32_t> r_slot;
+    std::vector<int64_t> r_gid;
+    std::vector<int32_t> r_rank;
+    for (size_t x = 0; x < ord.size(); ++x) {
+      if (x > 0 && cand[ord[x]].first == cand[ord[x - 1]].first) continue;
+      r_slot.push_back(cand[ord[x]].first);
+      r_gid.push_back(cand[ord[x]].second);
+      r_rank.push_back(cand_rank[ord[x]]);
+    }
+    // values served by this rank: owned LP rows (first copy = owner macro, local)
+    std::vector<std::pair<int64_t, uint32_t>> serve;
+    for (int64_t r = 0; r < nr; ++r) serve.push_back({rgid[r], copy[cp[r]]});
+    for (size_t fi = 0; fi < lv.h_flp.size(); ++fi) {
+      const FaceLP& F = lv.h_flp[fi];
+      for (int64_t q = 0; q < g.nfi; ++q) {
+        const int s = lv.h_fst[q] & 0xffff, t = lv.h_fst[q] >> 16;
+        int w[4] = {0, 0, 0, 0};
+        w[F.lA[0]] = N - s - t;
+        w[F.lA[1]] = s;
+        w[F.lA[2]] = t;
+        serve.push_back({g.base_f + F.fid * g.nfi + lv.h_fcidx[q], (uint32_t)slot_of(F.TA, w[1], w[2], w[3])});
+      }
+    }
+    std::sort(serve.begin(), serve.end());
+    hhg_status sp = dist_build_plan(c, lv, r_slot, r_gid, r_rank, serve);
+    if (sp != HHG_OK) return sp;
+  }
+  if (c->host_only) return HHG_OK;
+
   // ---- upload
   auto up = [&](auto*& dptr, const auto& vec) -> hhg_status {
     using T = typename std::remove_reference<decltype(vec)>::type::value_type;
@@ -419,7 +523,8 @@ static void free_level(Level& lv) {
   void* ps[] = {lv.d_row_ptr, lv.d_col, lv.d_val, lv.d_val_cons, lv.d_copy_ptr, lv.d_copy,
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
-                lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po};
+                lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
@@ -439,13 +544,25 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
   *out = nullptr;
   if (!vertices || !tets || !dirichlet_face || nv < 4 || nt < 1 || L_max < 2 || L_max > 8)
     return HHG_ERR_INVALID;
-  if (nranks != 1 || rank != 0) return HHG_ERR_INVALID;  // multi-rank: see DESIGN.md (next round)
-  (void)nccl_unique_id;
-  (void)macro_owner;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return HHG_ERR_INVALID;
+  if (macro_owner)
+    for (int64_t t = 0; t < nt; ++t)
+      if (macro_owner[t] < 0 || macro_owner[t] >= nranks) return HHG_ERR_INVALID;
   Ctx* c = new Ctx();
   c->stream = (cudaStream_t)cuda_stream;
   c->rank = rank;
   c->nranks = nranks;
+  c->owner.resize(nt);
+  for (int64_t t = 0; t < nt; ++t)
+    c->owner[t] = macro_owner ? macro_owner[t] : (int32_t)((t * nranks) / nt);
+  if (nranks > 1) {
+    hhg_status ts = dist_init_transport(c, nccl_unique_id);
+    if (ts != HHG_OK) {
+      fprintf(stderr, "hhg_setup_macro_mesh: transport: %s\n", c->err.c_str());
+      delete c;
+      return ts;
+    }
+  }
   c->L_max = L_max;
   c->nv = nv;
   c->nt = nt;
@@ -515,20 +632,11 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
   tp.fkey = fk;
   c->n_e = (int64_t)ek.size();
   c->n_f = (int64_t)fk.size();
-  // local macros (single rank: all)
-  c->nt_local = nt;
-  c->local_macros.resize(nt);
-  std::iota(c->local_macros.begin(), c->local_macros.end(), 0);
-  c->topo.resize(c->nt_local);
-  tp.vinc.assign(nv, {});
-  tp.einc.assign(c->n_e, {});
-  tp.finc.assign(c->n_f, {});
-  tp.vdir.assign(nv, 0);
-  tp.edir.assign(c->n_e, 0);
-  tp.fdir.assign(c->n_f, 0);
-  for (int64_t T = 0; T < c->nt_local; ++T) {
-    int64_t t = c->local_macros[T];
-    MacroTopo& m = c->topo[T];
+  // topology of every global macro
+  std::vector<MacroTopo> gtopo(nt);
+  std::vector<int> fcount(c->n_f, 0);
+  for (int64_t t = 0; t < nt; ++t) {
+    MacroTopo& m = gtopo[t];
     m.gT = t;
     for (int a = 0; a < 4; ++a) m.gv[a] = tets[4 * t + a];
     for (int a = 0; a < 4; ++a)
@@ -543,13 +651,57 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
         if (a != f) q[n++] = m.gv[a];
       std::sort(q, q + 3);
       m.f[f] = std::lower_bound(fk.begin(), fk.end(), (q[0] * nv + q[1]) * nv + q[2]) - fk.begin();
+      fcount[m.f[f]]++;
     }
+  }
+  for (int64_t f = 0; f < c->n_f; ++f)
+    if (fcount[f] > 2) return fail(HHG_ERR_MESH, "face shared by more than two tets");
+  // owner rank of every primitive = rank of the lowest-id macro containing it
+  tp.vown.assign(nv, -1);
+  tp.eown.assign(c->n_e, -1);
+  tp.fown.assign(c->n_f, -1);
+  for (int64_t t = nt - 1; t >= 0; --t) {
+    const MacroTopo& m = gtopo[t];
+    for (int a = 0; a < 4; ++a) tp.vown[m.gv[a]] = c->owner[t];
+    for (int e = 0; e < 6; ++e) tp.eown[m.e[e]] = c->owner[t];
+    for (int f = 0; f < 4; ++f) tp.fown[m.f[f]] = c->owner[t];
+  }
+  // blocks: local macros, then ghosts (other ranks' macros sharing a vertex with a local one)
+  std::vector<char> vlocal(nv, 0), isblk(nt, 0);
+  for (int64_t t = 0; t < nt; ++t)
+    if (c->owner[t] == rank)
+      for (int a = 0; a < 4; ++a) vlocal[gtopo[t].gv[a]] = 1;
+  c->local_macros.clear();
+  for (int64_t t = 0; t < nt; ++t)
+    if (c->owner[t] == rank) c->local_macros.push_back(t);
+  c->nt_local = (int64_t)c->local_macros.size();
+  for (int64_t t = 0; t < nt; ++t) {
+    if (c->owner[t] == rank) continue;
+    bool g = false;
+    for (int a = 0; a < 4; ++a) g = g || vlocal[gtopo[t].gv[a]];
+    if (g) c->local_macros.push_back(t);
+  }
+  c->nt_blocks = (int64_t)c->local_macros.size();
+  if (c->nt_local == 0) return fail(HHG_ERR_INVALID, "rank owns no macro");
+  c->g2b.assign(nt, -1);
+  for (int64_t T = 0; T < c->nt_blocks; ++T) c->g2b[c->local_macros[T]] = T;
+  c->topo.resize(c->nt_blocks);
+  for (int64_t T = 0; T < c->nt_blocks; ++T) c->topo[T] = gtopo[c->local_macros[T]];
+  // block incidence, ascending GLOBAL macro id (canonical summation order)
+  tp.vinc.assign(nv, {});
+  tp.einc.assign(c->n_e, {});
+  tp.finc.assign(c->n_f, {});
+  tp.vdir.assign(nv, 0);
+  tp.edir.assign(c->n_e, 0);
+  tp.fdir.assign(c->n_f, 0);
+  for (int64_t t = 0; t < nt; ++t) {
+    const int64_t T = c->g2b[t];
+    if (T < 0) continue;
+    const MacroTopo& m = c->topo[T];
     for (int a = 0; a < 4; ++a) tp.vinc[m.gv[a]].push_back((int32_t)T);
     for (int e = 0; e < 6; ++e) tp.einc[m.e[e]].push_back((int32_t)T);
     for (int f = 0; f < 4; ++f) tp.finc[m.f[f]].push_back((int32_t)T);
   }
-  for (int64_t f = 0; f < c->n_f; ++f)
-    if (tp.finc[f].size() > 2) return fail(HHG_ERR_MESH, "face shared by more than two tets");
   // primitive ownership (lowest local macro id) for the restriction R = P^T
   c->own.assign(c->nt_local, 0);
   for (int64_t T = 0; T < c->nt_local; ++T) {
@@ -563,9 +715,9 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
       if (tp.vinc[m.gv[v]][0] == T) o |= (uint16_t)(1u << (10 + v));
     c->own[T] = o;
   }
-  // Dirichlet closure
-  for (int64_t T = 0; T < c->nt_local; ++T) {
-    const MacroTopo& m = c->topo[T];
+  // Dirichlet closure (tags of every global macro)
+  for (int64_t t = 0; t < nt; ++t) {
+    const MacroTopo& m = gtopo[t];
     for (int f = 0; f < 4; ++f) {
       if (!dirichlet_face[4 * m.gT + f]) continue;
       tp.fdir[m.f[f]] = 1;
@@ -577,19 +729,21 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
       }
     }
   }
-  // ---- device geometry
-  std::vector<double> geo(c->nt_local * 16);
-  for (int64_t T = 0; T < c->nt_local; ++T)
+  // ---- device geometry (every block: ghost geometry feeds the face rows)
+  std::vector<double> geo(c->nt_blocks * 16);
+  for (int64_t T = 0; T < c->nt_blocks; ++T)
     for (int a = 0; a < 4; ++a) {
       int64_t v = c->topo[T].gv[a];
       for (int d = 0; d < 3; ++d) geo[T * 16 + 4 * a + d] = vertices[3 * v + d];
       geo[T * 16 + 4 * a + 3] = vertex_radius ? vertex_radius[v] : 0.0;
     }
-  cudaError_t e1 = cudaMalloc(&c->d_geo, geo.size() * sizeof(double));
-  if (e1 != cudaSuccess) return fail(HHG_ERR_CUDA, cudaGetErrorString(e1));
-  cudaMemcpy(c->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice);
-  cudaMalloc(&c->d_topo, c->topo.size() * sizeof(MacroTopo));
-  cudaMemcpy(c->d_topo, c->topo.data(), c->topo.size() * sizeof(MacroTopo), cudaMemcpyHostToDevice);
+  if (!c->host_only) {
+    cudaError_t e1 = cudaMalloc(&c->d_geo, geo.size() * sizeof(double));
+    if (e1 != cudaSuccess) return fail(HHG_ERR_CUDA, cudaGetErrorString(e1));
+    cudaMemcpy(c->d_geo, geo.data(), geo.size() * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMalloc(&c->d_topo, c->topo.size() * sizeof(MacroTopo));
+    cudaMemcpy(c->d_topo, c->topo.data(), c->topo.size() * sizeof(MacroTopo), cudaMemcpyHostToDevice);
+  }
   c->levels.resize(L_max + 1);
   for (int L = 2; L <= L_max; ++L) {
     hhg_status st = build_level(c, tp, L);
@@ -628,7 +782,12 @@ extern "C" int64_t hhg_kernel_launches(hhg_ctx ctx) {
 extern "C" void hhg_destroy(hhg_ctx ctx) {
   Ctx* c = (Ctx*)ctx;
   if (!c) return;
+  if (c->host_only) {
+    delete c;
+    return;
+  }
   cudaStreamSynchronize(c->stream);
+  dist_destroy(c);
   for (auto& lv : c->levels) free_level(lv);
   if (c->d_geo) cudaFree(c->d_geo);
   if (c->d_topo) cudaFree(c->d_topo);

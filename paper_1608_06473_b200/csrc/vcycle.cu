@@ -209,6 +209,8 @@ extern "C" hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coa
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: bad arguments");
   if (op != HHG_OP_SURROGATE && op != HHG_OP_CONST_AFFINE)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: smoother op must be SURROGATE or CONST_AFFINE");
+  if (c->nranks > 1 || c->host_only)
+    return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: single-rank contexts only in this version");
   for (int l = L_coarse; l <= L; ++l)
     if (!c->levels[l].fitted) return set_err(c, HHG_ERR_STATE, "hhg_vcycle: call hhg_fit_surrogates first");
   hhg_status st = ensure_mg(c);
