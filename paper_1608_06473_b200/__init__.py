@@ -164,6 +164,9 @@ class Ctx:
             except Exception:
                 stream = 0
         h = ctypes.c_void_p()
+        if nccl_id is not None:
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         st = L.hhg_setup_macro_mesh(v.ctypes.data, None if r is None else r.ctypes.data, v.shape[0],
                                     t.ctypes.data, t.shape[0], d.ctypes.data, int(L_max),
                                     None if o is None else o.ctypes.data, rank, nranks, nccl_id,
