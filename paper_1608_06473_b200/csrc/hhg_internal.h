@@ -183,6 +183,10 @@ struct Level {
   int* d_gs_flags = nullptr;   // [nt_local][n_bands][4] sweep epoch of completed colour passes
   int* d_gs_counter = nullptr; // [1]
   int gs_epoch = 0;
+  // static item schedule of the persistent kernels (pmarch.cuh), built on first use
+  int sched_grid = 0;
+  int* d_sched = nullptr;      // item ids, concatenated per CTA
+  int* d_sched_off = nullptr;  // [sched_grid + 1]
 };
 
 struct Ctx {

@@ -11,6 +11,8 @@
 #include "hhg_internal.h"
 #include "vol_kernels.cuh"
 #include "march.cuh"
+#include "pmarch.cuh"
+#include "pair.cuh"
 
 namespace hhg {
 
@@ -249,6 +251,99 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
   return HHG_OK;
 }
 
+// Persistent apply/residual (pmarch.cuh).  HHG_APPLY_KERNEL=march selects the
+// one-CTA-per-(macro,band) kernel above; p1 / p2 the persistent kernel with 1 / 2
+// nodes per thread step (default p2).
+static int apply_kernel_choice() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HHG_APPLY_KERNEL");
+    v = 0;
+    if (e && std::string(e) == "pair8") v = 5;
+    if (e && std::string(e) == "p1") v = 1;
+  }
+  return v;
+}
+
+// Persistent-grid size and the per-level static item schedule (pmarch.cuh).
+static hhg_status ensure_schedule(Ctx* c, Level& lv, const void* kernel, int& grid) {
+  static int g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    HHG_CK(c, cudaGetDevice(&dev));
+    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPThreads,
+                                                            pmarch_smem_bytes(24, 520, 256, 64)));
+    g = sms * std::max(per_sm, 1);
+  }
+  grid = g;
+  if (lv.sched_grid == grid) return HHG_OK;
+  std::vector<int> items, off;
+  build_pmarch_schedule(lv.bands, c->nt_local, grid, items, off);
+  if (lv.d_sched) cudaFree(lv.d_sched);
+  if (lv.d_sched_off) cudaFree(lv.d_sched_off);
+  HHG_CK(c, cudaMalloc(&lv.d_sched, std::max<size_t>(items.size(), 1) * sizeof(int)));
+  HHG_CK(c, cudaMalloc(&lv.d_sched_off, off.size() * sizeof(int)));
+  if (!items.empty())
+    HHG_CK(c, cudaMemcpy(lv.d_sched, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
+  HHG_CK(c, cudaMemcpy(lv.d_sched_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
+  lv.sched_grid = grid;
+  return HHG_OK;
+}
+
+template <int OP, int MODE, int NPS, int R>
+static hhg_status launch_pmarch(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
+  const int nb = (int)lv.bands.size();
+  const size_t smem = pmarch_smem_bytes(R, lv.slot_len, lv.N, nb);
+  static bool attr = false;
+  if (!attr) {
+    HHG_CK(c, cudaFuncSetAttribute(k_vol_pmarch<OP, MODE, NPS, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   112 * 1024));
+    attr = true;
+  }
+  if (smem > 112 * 1024) return set_err(c, HHG_ERR_INVALID, "pmarch: band too wide for shared memory");
+  int grid = 0;
+  hhg_status st = ensure_schedule(c, lv, (const void*)k_vol_pmarch<OP, MODE, NPS, R>, grid);
+  if (st != HHG_OK) return st;
+  ProfScope ps(c, 0);
+  k_vol_pmarch<OP, MODE, NPS, R><<<(unsigned)grid, kPThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, lv.d_sched, lv.d_sched_off);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+template <int OP, int MODE, int R>
+static hhg_status launch_pair(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
+  const int nb = (int)lv.bands.size();
+  const size_t smem = pair_smem_bytes(R, lv.slot_len, lv.N, nb);
+  static bool attr = false;
+  if (!attr) {
+    HHG_CK(c, cudaFuncSetAttribute(k_vol_pair<OP, MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   112 * 1024));
+    attr = true;
+  }
+  if (smem > 112 * 1024) return set_err(c, HHG_ERR_INVALID, "pair march: band too wide for shared memory");
+  int grid = 0;
+  hhg_status st = ensure_schedule(c, lv, (const void*)k_vol_pair<OP, MODE, R>, grid);
+  if (st != HHG_OK) return st;
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
+  ProfScope ps(c, 0);
+  k_vol_pair<OP, MODE, R><<<(unsigned)std::min<int64_t>(grid, c->nt_local * nb), kQThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, c->nt_local, lv.d_gs_counter);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+template <int OP, int MODE>
+static hhg_status launch_apply_vol(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
+  switch (apply_kernel_choice()) {
+    case 0: return launch_march<OP, MODE>(c, lv, u, f, out);
+    case 1: return launch_pmarch<OP, MODE, 1, 16>(c, lv, u, f, out);
+    case 5: return launch_pair<OP, MODE, 8>(c, lv, u, f, out);
+    default: return launch_march<OP, MODE>(c, lv, u, f, out);
+  }
+}
+
 template <int OP>
 static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, const double* f) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
@@ -308,12 +403,12 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
   }
   if (mode != kModeGS && !force_v1() && !lv.bands.empty()) {
     if (op == HHG_OP_SURROGATE && lv.d_coef10) {
-      return mode == kModeApply ? launch_march<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out)
-                                : launch_march<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out);
+      return mode == kModeApply ? launch_apply_vol<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out)
+                                : launch_apply_vol<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out);
     }
     if (op == HHG_OP_CONST_AFFINE) {
-      return mode == kModeApply ? launch_march<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
-                                : launch_march<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
+      return mode == kModeApply ? launch_apply_vol<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
+                                : launch_apply_vol<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
     }
   }
   dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
