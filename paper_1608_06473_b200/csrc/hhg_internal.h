@@ -108,6 +108,7 @@ struct Band {
   int ncolumns;     // interior columns (threads used)
 };
 constexpr int kMarchThreads = 256;
+constexpr int kNarrowThreads = 128;
 constexpr int kRing = 16;  // plane slots (power of 2); >= 11 planes in flight ahead of use
 
 // Structured lower-primitive rows of one non-Dirichlet macro face (faces.cu).
@@ -153,10 +154,14 @@ struct Level {
   double* d_cons = nullptr;        // [nt_local][15] affine constant stencil
   double* d_coef10 = nullptr;      // [nt_local][15][10] q<=2 coefficients zero-padded to q=2
   bool fitted = false;
-  // column-march bands
+  // column-march bands (<= kMarchThreads columns) and narrow bands (<= kNarrowThreads)
   std::vector<Band> bands;
   Band* d_bands = nullptr;
   int slot_len = 0;
+  std::vector<Band> bands_s;
+  Band* d_bands_s = nullptr;
+  int slot_len_s = 0;
+  int* d_gs_flags_s = nullptr;
   // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order
   int64_t n_flp = 0, n_frows = 0;
   int fcol[4] = {0, 0, 0, 0};      // colour offsets of q ((s+2t) mod 3 = 0,1,2)

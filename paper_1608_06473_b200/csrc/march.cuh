@@ -304,22 +304,27 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int 
       const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
                              Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
-      double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      double r;
       if (OP == HHG_OP_SURROGATE) {
+        // expanded weight polynomial: three independent accumulation chains
+        double x = 0.0, y = 0.0, z = 0.0;
 #pragma unroll
         for (int w = 0; w < 15; ++w) {
           if (w == kMC) continue;
-          const double sw = fma(fma(sm.Cw[w], kd, B[w]), kd, A[w]);
-          acc[w % 5] = fma(sw, uu[w], acc[w % 5]);
+          x = fma(A[w], uu[w], x);
+          y = fma(B[w], uu[w], y);
+          z = fma(sm.Cw[w], uu[w], z);
         }
+        r = fma(fma(z, kd, y), kd, x);
       } else {
+        double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
         for (int w = 0; w < 15; ++w) {
           if (w == kMC) continue;
-          acc[w % 5] = fma(A[w], uu[w], acc[w % 5]);
+          acc[w % 3] = fma(A[w], uu[w], acc[w % 3]);
         }
+        r = (acc[0] + acc[1]) + acc[2];
       }
-      const double r = (acc[0] + acc[1]) + (acc[2] + acc[3]) + acc[4];
       wb[sm.po[k]] = (fv - r) * rinv;
     }
     // every 3 steps: all warps done with planes <= 4s+2 (next step reads >= 4s+3);
@@ -373,8 +378,8 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // running yet; every other running item's neighbours run too => no deadlock
 // while the grid has more CTAs than a macro has bands.
 // ---------------------------------------------------------------------------
-template <int OP>
-__global__ void __launch_bounds__(kMarchThreads, 2)
+template <int OP, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
                const double* __restrict__ f, int64_t ntl, int G, int* __restrict__ counter,

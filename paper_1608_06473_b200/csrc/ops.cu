@@ -13,6 +13,7 @@
 #include "march.cuh"
 #include "pmarch.cuh"
 #include "pair.cuh"
+#include "gsq.cuh"
 
 namespace hhg {
 
@@ -360,20 +361,25 @@ static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, cons
   return HHG_OK;
 }
 
-template <int OP>
-static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f) {
-  const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
+template <int OP, int NT>
+static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double* f) {
+  const bool narrow = NT == kNarrowThreads;
+  const std::vector<Band>& bands = narrow ? lv.bands_s : lv.bands;
+  const Band* d_bands = narrow ? lv.d_bands_s : lv.d_bands;
+  int* flags = narrow ? lv.d_gs_flags_s : lv.d_gs_flags;
+  const int slot_len = narrow ? lv.slot_len_s : lv.slot_len;
+  const size_t smem = march_smem_bytes(slot_len, lv.N);
   static int grid = 0;
   if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
     int dev = 0, sms = 0, per_sm = 0;
     HHG_CK(c, cudaGetDevice(&dev));
     HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP>, kMarchThreads,
-                                                            march_smem_bytes(520, 256)));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT>, NT,
+                                                            march_smem_bytes(narrow ? 400 : 520, 256)));
     grid = sms * std::max(per_sm, 1);
   }
-  const int nb = (int)lv.bands.size();
+  const int nb = (int)bands.size();
   // macro group: u and f of G macros (~90 MB) stay L2-resident across the 4
   // colours, and a colour stage (G x bands items) is several CTA waves long so
   // that stage c+1 rarely waits for stage c.
@@ -388,9 +394,51 @@ static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f)
   HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
   const int64_t items = c->nt_local * nb;
   ProfScope ps(c, 1);
-  k_gs_items<OP><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G,
-      lv.d_gs_counter, lv.d_gs_flags, lv.gs_epoch);
+  k_gs_items<OP, NT><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+      lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G, lv.d_gs_counter, flags,
+      lv.gs_epoch);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+template <int OP>
+static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f) {
+  static int nt = -1;
+  if (nt < 0) {
+    const char* e = getenv("HHG_GS_CTA");
+    nt = (e && atoi(e) == 128) ? 128 : 256;
+  }
+  if (nt == 128 && !lv.bands_s.empty()) return launch_gs_items_nt<OP, kNarrowThreads>(c, lv, u, f);
+  return launch_gs_items_nt<OP, kMarchThreads>(c, lv, u, f);
+}
+
+// Whole volume GS sweep as one continuously pipelined persistent launch (gsq.cuh).
+template <int OP>
+static hhg_status launch_gs_quad(Ctx* c, Level& lv, double* u, const double* f) {
+  const size_t smem = gsq_smem_bytes(lv.slot_len, lv.N);
+  static int grid = 0;
+  if (grid == 0) {
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_quad<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    int dev = 0, sms = 0, per_sm = 0;
+    HHG_CK(c, cudaGetDevice(&dev));
+    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_quad<OP>, kGThreads,
+                                                            gsq_smem_bytes(520, 256)));
+    grid = sms * std::max(per_sm, 1);
+  }
+  if (smem > 110 * 1024) return set_err(c, HHG_ERR_INVALID, "gs: band too wide for shared memory");
+  const int nb = (int)lv.bands.size();
+  if (lv.gs_epoch >= 200000) {  // progress words encode epoch * 8192: restart the epochs
+    HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
+    lv.gs_epoch = 0;
+  }
+  lv.gs_epoch += 1;
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
+  const int64_t items = c->nt_local * nb;
+  ProfScope ps(c, 1);
+  k_gs_quad<OP><<<(unsigned)std::min<int64_t>(grid, items), kGThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter,
+      lv.d_gs_flags, lv.gs_epoch);
   HHG_LAUNCHED(c);
   return HHG_OK;
 }
@@ -504,14 +552,18 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
     hhg_status sts = dist_sync(c, lv, u);
     if (sts != HHG_OK) return sts;
   }
-  static int mode = -1;  // HHG_GS_KERNEL=passes -> 4 colour launches
+  static int mode = -1;  // HHG_GS_KERNEL: passes -> 4 colour launches, quad -> k_gs_quad, default k_gs_items
   if (mode < 0) {
     const char* e = getenv("HHG_GS_KERNEL");
-    mode = (e && std::string(e) == "passes") ? 1 : 0;
+    mode = (e && std::string(e) == "passes") ? 1 : (e && std::string(e) == "quad") ? 0 : 2;
   }
   const bool march_ok = !force_v1() && !lv.bands.empty() &&
                         ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
   if (march_ok && mode == 0) {
+    hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_quad<HHG_OP_SURROGATE>(c, lv, u, f)
+                                           : launch_gs_quad<HHG_OP_CONST_AFFINE>(c, lv, u, f);
+    if (st != HHG_OK) return st;
+  } else if (march_ok && mode == 2) {
     hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
                                            : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
     if (st != HHG_OK) return st;
@@ -708,3 +760,12 @@ extern "C" hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, 
   c->ev_rec[kind].clear();
   return HHG_OK;
 }
+
+#ifdef HHG_GS_PROF
+extern "C" int hhg_gs_prof_read(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, hhg::g_gsprof, 8 * sizeof(unsigned long long));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(hhg::g_gsprof, z, sizeof(z));
+  return 0;
+}
+#endif

@@ -171,23 +171,29 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   lv.N = N;
   lv.P = n_lattice(N);
   lv.S = (lv.P + 2 + 31) / 32 * 32;  // >= P+2: 16-byte-rounded bulk copies stay inside the block
-  // column-march bands: consecutive diagonals with <= kMarchThreads interior columns
-  lv.bands.clear();
-  lv.slot_len = 0;
-  for (int d = 2; d <= N - 2;) {
-    Band b{};
-    b.d0 = d;
-    int cnt = 0;
-    while (d <= N - 2 && cnt + (d - 1) <= kMarchThreads) cnt += d - 1, ++d;
-    if (cnt == 0) return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA");
-    b.d1 = d;
-    b.ncolumns = cnt;
-    b.c_lo = (int)col_idx(b.d0 - 1, 0);
-    b.ncols = (int)col_idx(0, b.d1) + 1 - b.c_lo;  // through the end of diagonal d1
-    b.kmax = N - 1 - b.d0;
-    lv.bands.push_back(b);
-    lv.slot_len = std::max(lv.slot_len, (b.ncols + 2 + 3) / 4 * 4);
-  }
+  // column-march bands: consecutive diagonals with <= W interior columns
+  auto make_bands = [&](int W, std::vector<Band>& out, int& slot_len) -> bool {
+    out.clear();
+    slot_len = 0;
+    for (int d = 2; d <= N - 2;) {
+      Band b{};
+      b.d0 = d;
+      int cnt = 0;
+      while (d <= N - 2 && cnt + (d - 1) <= W) cnt += d - 1, ++d;
+      if (cnt == 0) return false;
+      b.d1 = d;
+      b.ncolumns = cnt;
+      b.c_lo = (int)col_idx(b.d0 - 1, 0);
+      b.ncols = (int)col_idx(0, b.d1) + 1 - b.c_lo;  // through the end of diagonal d1
+      b.kmax = N - 1 - b.d0;
+      out.push_back(b);
+      slot_len = std::max(slot_len, (b.ncols + 2 + 3) / 4 * 4);
+    }
+    return true;
+  };
+  if (!make_bands(kMarchThreads, lv.bands, lv.slot_len))
+    return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA");
+  if (!make_bands(kNarrowThreads, lv.bands_s, lv.slot_len_s)) lv.bands_s.clear();  // N > 129: not used
   lv.n_local = lv.S * c->nt_blocks;
   GidInfo& g = lv.gi;
   g.N = N;
@@ -495,10 +501,14 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if ((st = up(lv.d_dir_slot, dslot)) != HHG_OK) return st;
   if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
   if ((st = up(lv.d_bands, lv.bands)) != HHG_OK) return st;
+  if ((st = up(lv.d_bands_s, lv.bands_s)) != HHG_OK) return st;
   {
     const size_t nfl = (size_t)c->nt_local * std::max<size_t>(lv.bands.size(), 1) * 4;
     HHG_CK(c, cudaMalloc(&lv.d_gs_flags, nfl * sizeof(int)));
     HHG_CK(c, cudaMemset(lv.d_gs_flags, 0, nfl * sizeof(int)));
+    const size_t nfs = (size_t)c->nt_local * std::max<size_t>(lv.bands_s.size(), 1) * 4;
+    HHG_CK(c, cudaMalloc(&lv.d_gs_flags_s, nfs * sizeof(int)));
+    HHG_CK(c, cudaMemset(lv.d_gs_flags_s, 0, nfs * sizeof(int)));
     HHG_CK(c, cudaMalloc(&lv.d_gs_counter, sizeof(int)));
   }
   HHG_CK(c, cudaMalloc(&lv.d_val, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
@@ -524,7 +534,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
