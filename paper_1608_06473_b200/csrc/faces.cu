@@ -34,9 +34,9 @@ __global__ void k_face_values(const double* __restrict__ geo, int N, int64_t nfi
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n_frows) return;
   const int64_t f = r / nfi;
-  const uint32_t st = fst[r - f * nfi];
-  const int s = st & 0xffff, t = st >> 16;
   const FaceLP F = flp[f];
+  const uint32_t st = fst[F.z * nfi + (r - f * nfi)];
+  const int s = st & 0xffff, t = st >> 16;
   double acc[15];
   for (int e = 0; e < 15; ++e) acc[e] = 0.0;
   for (int side = 0; side < 2; ++side) {
@@ -106,8 +106,8 @@ __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, con
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n_frows) return;
   const int64_t fc = r / nfi;
-  const uint32_t st = fst[r - fc * nfi];
   const FaceLP& F = flp[fc];
+  const uint32_t st = fst[F.z * nfi + (r - fc * nfi)];
   FaceRowSlots o;
   face_row_slots(F, N, S, po_s, st & 0xffff, st >> 16, o);
   double acc = val[r] * u[o.cA];
@@ -119,10 +119,19 @@ __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, con
   if (o.cB >= 0) out[o.cB] = res;
 }
 
-// GS colour step on face nodes of colour `colour`: compute into tmp, then write.
+// A face node whose (s,t) is at least 2 away from the face's edges has no
+// neighbour outside its own face and the two adjacent volumes, and nodes of one
+// face colour are never neighbours inside a face: such nodes can be updated in
+// place within a colour step without changing its simultaneous-update
+// semantics (R13).  Nodes next to an edge may neighbour same-colour
+// nodes of another face (through the volume), so they go through tmp.
+__device__ __forceinline__ bool face_inner(int N, int s, int t) { return s >= 2 && t >= 2 && s + t <= N - 2; }
+
+// GS colour step on face nodes of colour `colour`: inner nodes in place,
+// near-edge nodes into tmp (written by k_face_write after the step).
 __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, const FaceLP* __restrict__ flp,
                           const uint32_t* __restrict__ fst, const int* __restrict__ po, int64_t n_frows,
-                          const double* __restrict__ val, const double* __restrict__ u,
+                          const double* __restrict__ val, double* __restrict__ u,
                           const double* __restrict__ f, double* __restrict__ tmp) {
   __shared__ int po_s[260];
   load_po(po_s, po, N);
@@ -132,15 +141,21 @@ __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, co
   if (x >= per_face * (n_frows / nfi)) return;
   const int64_t q = q0 + (x - fc * per_face);
   const int64_t r = fc * nfi + q;
-  const uint32_t st = fst[q];
   const FaceLP& F = flp[fc];
+  const uint32_t st = fst[F.z * nfi + q];
   FaceRowSlots o;
   face_row_slots(F, N, S, po_s, st & 0xffff, st >> 16, o);
   double acc = f[o.cA];
 #pragma unroll
   for (int e = 0; e < 14; ++e)
     if (o.nb[e] >= 0) acc = fma(-val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
-  tmp[r] = acc / val[r];
+  const double v = acc / val[r];
+  if (face_inner(N, st & 0xffff, st >> 16)) {
+    u[o.cA] = v;
+    if (o.cB >= 0) u[o.cB] = v;
+  } else {
+    tmp[r] = v;
+  }
 }
 
 __global__ void k_face_write(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, const FaceLP* __restrict__ flp,
@@ -152,9 +167,10 @@ __global__ void k_face_write(int N, int64_t S, int64_t nfi, int64_t nfc, int q0,
   const int64_t fc = x / nfc;
   if (fc >= n_faces) return;
   const int64_t q = q0 + (x - fc * nfc);
-  const uint32_t st = fst[q];
   const FaceLP& F = flp[fc];
+  const uint32_t st = fst[F.z * nfi + q];
   const int s = st & 0xffff, t = st >> 16;
+  if (face_inner(N, s, t)) return;  // updated in place by k_face_gs
   const FaceNode a = face_node(F.lA, N, s, t);
   const double v = tmp[fc * nfi + q];
   u[fslot(F.TA, S, po_s, a.i, a.j, a.k)] = v;
@@ -175,8 +191,8 @@ __global__ void k_face_gather(int N, int64_t S, int64_t nfi, int64_t n_frows, co
   if (r >= n_frows) return;
   const int64_t fc = r / nfi;
   const int64_t q = r - fc * nfi;
-  const uint32_t st = fst[q];
   const FaceLP& F = flp[fc];
+  const uint32_t st = fst[F.z * nfi + q];
   const int s = st & 0xffff, t = st >> 16;
   const FaceNode a = face_node(F.lA, N, s, t);
   const int64_t sA = fslot(F.TA, S, po_s, a.i, a.j, a.k);
@@ -185,7 +201,7 @@ __global__ void k_face_gather(int N, int64_t S, int64_t nfi, int64_t n_frows, co
     const FaceNode b = face_node(F.lB, N, s, t);
     sB = fslot(F.TB, S, po_s, b.i, b.j, b.k);
   }
-  const int64_t g = base_f + F.fid * nfi + fcidx[q];
+  const int64_t g = base_f + F.fid * nfi + fcidx[F.z * nfi + q];
   if (dir == 0) {
     glob[g] = local[sA];
   } else {
@@ -205,8 +221,8 @@ __global__ void k_face_dot(int N, int64_t S, int64_t nfi, int64_t n_frows, const
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_frows;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t fc = r / nfi;
-    const uint32_t st = fst[r - fc * nfi];
     const FaceLP& F = flp[fc];
+    const uint32_t st = fst[F.z * nfi + (r - fc * nfi)];
     const FaceNode a = face_node(F.lA, N, st & 0xffff, st >> 16);
     const int64_t sl = fslot(F.TA, S, po_s, a.i, a.j, a.k);
     acc += av[sl] * bv[sl];
@@ -279,8 +295,8 @@ __global__ void k_face_sumcopies(int N, int64_t S, int64_t nfi, int64_t n_frows,
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n_frows) return;
   const int64_t fc = r / nfi;
-  const uint32_t st = fst[r - fc * nfi];
   const FaceLP& F = flp[fc];
+  const uint32_t st = fst[F.z * nfi + (r - fc * nfi)];
   if (F.TB < 0) return;
   const int s = st & 0xffff, t = st >> 16;
   const FaceNode a = face_node(F.lA, N, s, t), b = face_node(F.lB, N, s, t);

@@ -127,6 +127,8 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
   auto make10 = [&](Level& lv) -> hhg_status {
     if (lv.d_coef10) cudaFree(lv.d_coef10);
     lv.d_coef10 = nullptr;
+    if (lv.d_cC) cudaFree(lv.d_cC);  // derived from d_coef10 on first use (ops.cu)
+    lv.d_cC = nullptr;
     if (q > 2) return HHG_OK;
     HHG_CK(c, cudaMalloc(&lv.d_coef10, c->nt_local * 150 * sizeof(double)));
     HHG_CK(c, cudaMemsetAsync(lv.d_coef10, 0, c->nt_local * 150 * sizeof(double), c->stream));

@@ -119,6 +119,7 @@ struct FaceLP {
   int8_t lA[3], lB[3];  // local vertex of the face's sorted vertices a<b<c in A / B
   int8_t off[14][3];    // ijk offsets: [0..5] in-face (A frame), [6..9] into A, [10..13] into B (B frame)
   int8_t mapA[15], mapB[15];  // partial-stencil direction -> entry (-1: not a neighbour)
+  int8_t z;             // in-face row mode: node order q -> (s,t) from table fst[z] (setup.cu)
   int64_t fid;          // canonical face id
 };
 
@@ -153,6 +154,7 @@ struct Level {
   double* d_coef = nullptr;        // [nt_local][15][mq] index units, exponent order kExp
   double* d_cons = nullptr;        // [nt_local][15] affine constant stencil
   double* d_coef10 = nullptr;      // [nt_local][15][10] q<=2 coefficients zero-padded to q=2
+  double* d_cC = nullptr;          // [nt_local][15] k^2 coefficients (coef10[..][9]), march kernels
   bool fitted = false;
   // column-march bands (<= kMarchThreads columns) and narrow bands (<= kNarrowThreads)
   std::vector<Band> bands;
@@ -166,8 +168,8 @@ struct Level {
   int64_t n_flp = 0, n_frows = 0;
   int fcol[4] = {0, 0, 0, 0};      // colour offsets of q ((s+2t) mod 3 = 0,1,2)
   FaceLP* d_flp = nullptr;
-  uint32_t* d_fst = nullptr;       // [nfi] s | t << 16 for q
-  int* d_fcidx = nullptr;          // [nfi] canonical in-face index of q
+  uint32_t* d_fst = nullptr;       // [3][nfi] s | t << 16 for q, per row mode z
+  int* d_fcidx = nullptr;          // [3][nfi] canonical in-face index of q
   double* d_fval = nullptr;        // [15][n_frows] exact FEM, blended
   double* d_fval_cons = nullptr;   // [15][n_frows] exact FEM, affine
   double* d_ftmp = nullptr;        // [n_frows] GS scratch

@@ -178,15 +178,23 @@ __device__ __forceinline__ void march_prologue(MarchSmem& sm, const Band& b, int
 // ---------------------------------------------------------------------------
 // apply / residual: march k = 1..len, one node per step, 7 new shared loads
 // ---------------------------------------------------------------------------
+// k^2 coefficients C_w (= c_002 of weight w) of up to kCMax macros [T - T0][15],
+// uploaded per launch chunk.  T is uniform in the non-persistent march kernel
+// (blockIdx), so the compiler keeps the 15 C_w of the CTA's macro in uniform
+// registers and feeds them to DFMA directly (no per-node shared loads).
+constexpr int kCMax = 512;
+__constant__ double g_cC[kCMax * 15];
+
 template <int OP, int MODE>
 __global__ void __launch_bounds__(kMarchThreads, 2)
     k_vol_march(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                 const double* __restrict__ coef10, const double* __restrict__ cons,
-                const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out) {
+                const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out, int T0) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem sm(smem, slot_len);
-  const int64_t T = blockIdx.x / n_bands;
-  const Band b = bands[blockIdx.x - T * n_bands];
+  const int Tl = blockIdx.x / n_bands;  // macro within the launch chunk (uniform)
+  const int64_t T = T0 + Tl;
+  const Band b = bands[blockIdx.x - Tl * n_bands];
   const double* ub = u + T * S;
   const Column q = make_column(b, N);
   double A[15], B[15];
@@ -229,7 +237,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
         const double kd = (double)k;
 #pragma unroll
         for (int w = 0; w < 15; ++w) {
-          const double s = fma(fma(sm.Cw[w], kd, B[w]), kd, A[w]);
+          const double s = fma(fma(g_cC[Tl * 15 + w], kd, B[w]), kd, A[w]);
           acc[w % 5] = fma(s, uu[w], acc[w % 5]);
         }
       } else {
@@ -259,11 +267,50 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // thread visits its colour-c nodes k = delta + 4s (one per step of 4 planes).
 // The column coefficients (A, B) are computed by the caller once per band.
 // ---------------------------------------------------------------------------
-template <int OP>
+struct NoGate {
+  __device__ void wait(int) const {}
+  __device__ void publish(int) const {}
+};
+
+// Gate/publisher of the progress-gated GS (k_gs_items_p): before warp 0 issues
+// planes <= `to` of pass c, the two neighbour bands must have finished pass
+// c-1 up to plane to+1; after each refill barrier the band publishes how many
+// planes of pass c are done.
+struct ProgGate {
+  int* mine;            // own progress word
+  const int* left;      // neighbour words (nullptr: no neighbour)
+  const int* right;
+  int base;             // epoch * 8192
+  int colour;
+  __device__ void wait(int to) const {
+    if (colour == 0) return;
+    if (threadIdx.x == 0) {
+      const int want = base + (colour - 1) * 1024 + to + 2;
+      for (;;) {
+        int v = 0x7fffffff;
+        if (left) v = min(v, *(const volatile int*)left);
+        if (right) v = min(v, *(const volatile int*)right);
+        if (v >= want) break;
+        __nanosleep(64);
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    __syncwarp();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  // called by all threads right after a __syncthreads
+  // (by the last warp: the release fence must not delay warp 0, the TMA issuer)
+  __device__ void publish(int done) const {
+    if (threadIdx.x == blockDim.x - 32)
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(mine), "r"(base + done) : "memory");
+  }
+};
+
+template <int OP, class Gate = NoGate>
 __device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int N, const Band& b, const Column& q,
                                                const double (&A)[15], const double (&B)[15], int colour,
                                                double* __restrict__ ub, const double* __restrict__ fb,
-                                               double* __restrict__ wb) {
+                                               double* __restrict__ wb, const Gate& gate = Gate()) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) mbar_init(&sm.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -273,6 +320,7 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int 
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
   const int last_plane = b.kmax + 1;
   int next_issue = min(kRing, last_plane + 1);
+  if (threadIdx.x < 32) gate.wait(next_issue - 1);
   issue_planes(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
   const int clo = b.c_lo;
   auto sptr = [&](int p) -> const double* {
@@ -331,7 +379,9 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int 
     // refill up to plane 4s+18 (the following 3 steps need <= 4s+16).
     if (s % 3 == 2 || s == nsteps - 1) {
       __syncthreads();
+      gate.publish(colour * 1024 + min(4 * s + 4, last_plane + 1));
       const int to = min(4 * s + 2 + kRing, last_plane);
+      if (to >= next_issue && threadIdx.x < 32) gate.wait(to);
       issue_planes(ub, sm.po, next_issue, to, b, sm.ring, slot_len, sm.bars);
       next_issue = max(next_issue, to + 1);
     }
@@ -416,6 +466,46 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       __threadfence();
       __syncthreads();
       if (threadIdx.x == 0) atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
+    }
+  }
+}
+
+// Same items and colour passes, but with PLANE-level dependencies: pass c of
+// band b may load plane p as soon as bands b-1, b+1 have finished pass c-1 up
+// to plane p+1 (each band publishes its progress at every ring refill), so a
+// pass overlaps the tail of its neighbours' previous pass instead of waiting
+// for their completion.  prog[T][b] = epoch * 8192 + pass * 1024 + planes done.
+template <int OP, int NT>
+__global__ void __launch_bounds__(NT, 512 / NT)
+    k_gs_items_p(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
+                 const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
+                 const double* __restrict__ f, int64_t ntl, int* __restrict__ counter, int* __restrict__ prog,
+                 int epoch) {
+  extern __shared__ __align__(16) double smem[];
+  MarchSmem sm(smem, slot_len);
+  __shared__ int s_item;
+  const int64_t total = ntl * n_bands;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const int64_t T = item / n_bands;
+    const int band = (int)(item - T * n_bands);
+    const Band b = bands[band];
+    Column q;
+    double A[15], B[15];
+    band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
+    int* row = prog + T * n_bands;
+    ProgGate gate{row + band, band > 0 ? row + band - 1 : nullptr, band + 1 < n_bands ? row + band + 1 : nullptr,
+                  epoch * 8192, 0};
+    for (int colour = 0; colour < 4; ++colour) {
+      gate.colour = colour;
+      if (colour > 0 && threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
+      gs_colour_pass<OP>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c, gate);
+      __syncthreads();
+      gate.publish((colour + 1) * 1024);
     }
   }
 }

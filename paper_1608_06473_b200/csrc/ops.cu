@@ -245,10 +245,21 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
     attr = true;
   }
   const int nb = (int)lv.bands.size();
+  if (OP == HHG_OP_SURROGATE && !lv.d_cC) {  // C_w = coefficient 9 of each weight polynomial
+    HHG_CK(c, cudaMalloc(&lv.d_cC, (size_t)c->nt_local * 15 * sizeof(double)));
+    HHG_CK(c, cudaMemcpy2DAsync(lv.d_cC, sizeof(double), lv.d_coef10 + 9, 10 * sizeof(double), sizeof(double),
+                                (size_t)c->nt_local * 15, cudaMemcpyDeviceToDevice, c->stream));
+  }
   ProfScope ps(c, 0);
-  k_vol_march<OP, MODE><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out);
-  HHG_LAUNCHED(c);
+  for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
+    const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
+    if (OP == HHG_OP_SURROGATE)
+      HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+    k_vol_march<OP, MODE><<<(unsigned)(nb * nt), kMarchThreads, smem, c->stream>>>(
+        lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, (int)T0);
+    HHG_LAUNCHED(c);
+  }
   return HHG_OK;
 }
 
@@ -390,13 +401,34 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
     l2_target = e ? atof(e) * 1e6 : 90.0e6;
   }
   int G = (int)std::max(1.0, std::min((double)c->nt_local, l2_target / per_macro));
+  static int gated = -1;  // HHG_GS_DEPS=gate -> plane-level progress gating (k_gs_items_p; measured slower)
+  if (gated < 0) {
+    const char* e = getenv("HHG_GS_DEPS");
+    gated = (e && std::string(e) == "gate") ? 1 : 0;
+  }
+  if (gated && lv.gs_epoch >= 200000) {  // progress words encode epoch * 8192
+    HHG_CK(c, cudaMemsetAsync(flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
+    lv.gs_epoch = 0;
+  }
   lv.gs_epoch += 1;
   HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
   const int64_t items = c->nt_local * nb;
   ProfScope ps(c, 1);
-  k_gs_items<OP, NT><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
-      lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G, lv.d_gs_counter, flags,
-      lv.gs_epoch);
+  if (gated) {
+    static bool attr = false;
+    if (!attr) {
+      HHG_CK(c, cudaFuncSetAttribute(k_gs_items_p<OP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     110 * 1024));
+      attr = true;
+    }
+    k_gs_items_p<OP, NT><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+        lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter, flags,
+        lv.gs_epoch);
+  } else {
+    k_gs_items<OP, NT><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+        lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G, lv.d_gs_counter, flags,
+        lv.gs_epoch);
+  }
   HHG_LAUNCHED(c);
   return HHG_OK;
 }

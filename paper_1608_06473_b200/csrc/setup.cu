@@ -78,20 +78,33 @@ static int local_of(const int64_t* tv, int64_t g) {
 static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
   const int N = lv.N;
   const int64_t nfi = lv.gi.nfi;
-  // in-face node order: colour-major ((s+2t) mod 3), then canonical (t outer, s inner)
+  // In-face node orders, one per "row mode" z in {0,1,2}: colour-major
+  // ((s+2t) mod 3, the face colouring of the GS class steps), then rows of
+  // constant weight w_z on the face's z-th sorted vertex, inner index moving
+  // weight between the two other vertices.  A face uses the mode whose inner
+  // direction stays inside one lattice plane of its primary macro (contiguous
+  // along a diagonal when the face contains local vertices 1 and 2), so
+  // consecutive threads touch neighbouring addresses.
   std::vector<uint32_t> fst;
   std::vector<int> fcidx;
-  for (int col = 0; col < 3; ++col) {
-    lv.fcol[col] = (int)fst.size();
-    int ci = 0;
-    for (int t = 1; t <= N - 2; ++t)
-      for (int s = 1; s <= N - 1 - t; ++s, ++ci)
-        if ((s + 2 * t) % 3 == col) {
+  for (int z = 0; z < 3; ++z) {
+    const int x = z == 0 ? 1 : 0, y = z == 2 ? 1 : 2;
+    for (int col = 0; col < 3; ++col) {
+      if (z == 0) lv.fcol[col] = (int)(fst.size());
+      for (int wz = 1; wz <= N - 2; ++wz)
+        for (int wy = 1; wy <= N - 1 - wz; ++wy) {
+          int w[3];
+          w[z] = wz;
+          w[y] = wy;
+          w[x] = N - wz - wy;
+          const int s = w[1], t = w[2];
+          if ((s + 2 * t) % 3 != col) continue;
           fst.push_back((uint32_t)s | ((uint32_t)t << 16));
-          fcidx.push_back(ci);
+          fcidx.push_back((t - 1) * (N - 1) - (t - 1) * t / 2 + (s - 1));
         }
+    }
+    if (z == 0) lv.fcol[3] = (int)fst.size();
   }
-  lv.fcol[3] = (int)fst.size();
   const int D[6][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {-1, 1}, {1, -1}};
   std::vector<FaceLP> flp;
   for (int64_t f = 0; f < c->n_f; ++f) {
@@ -103,6 +116,18 @@ static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
     F.fid = f;
     F.TA = tp.finc[f][0];
     F.TB = tp.finc[f].size() > 1 ? tp.finc[f][1] : -1;
+    {
+      // primary frame: prefer the macro in which the face contains local vertices 1 and 2
+      // (contiguous rows); only swap between two local macros (the exchange plan serves A)
+      auto opp = [&](int T) {
+        const int64_t* gv = c->topo[T].gv;
+        return 6 - local_of(gv, va) - local_of(gv, vb) - local_of(gv, vc);
+      };
+      if (F.TB >= 0 && F.TA < c->nt_local && F.TB < c->nt_local) {
+        const int la = opp(F.TA), lb = opp(F.TB);
+        if ((la == 1 || la == 2) && (lb == 0 || lb == 3)) std::swap(F.TA, F.TB);
+      }
+    }
     for (int side = 0; side < 2; ++side) {
       const int T = side == 0 ? F.TA : F.TB;
       int8_t* l = side == 0 ? F.lA : F.lB;
@@ -132,6 +157,13 @@ static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
         }
       }
       if (n_into != 4) return set_err(c, HHG_ERR_MESH, "face with != 4 into-macro directions");
+    }
+    {
+      const int lf = 6 - F.lA[0] - F.lA[1] - F.lA[2];
+      const int want = lf == 3 ? 0 : 3;  // hold the weight of local vertex 0 (k=0 face) or 3 (keep k)
+      F.z = 0;
+      for (int p = 0; p < 3; ++p)
+        if (F.lA[p] == want) F.z = (int8_t)p;
     }
     flp.push_back(F);
   }
@@ -424,7 +456,7 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
     for (const FaceLP& F : lv.h_flp) {
       if (F.TB < c->nt_local) continue;
       for (int64_t q = 0; q < g.nfi; ++q) {
-        const int s = lv.h_fst[q] & 0xffff, t = lv.h_fst[q] >> 16;
+        const int s = lv.h_fst[F.z * g.nfi + q] & 0xffff, t = lv.h_fst[F.z * g.nfi + q] >> 16;
         int w[4] = {0, 0, 0, 0};
         w[F.lB[0]] = N - s - t;
         w[F.lB[1]] = s;
@@ -469,12 +501,13 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
     for (size_t fi = 0; fi < lv.h_flp.size(); ++fi) {
       const FaceLP& F = lv.h_flp[fi];
       for (int64_t q = 0; q < g.nfi; ++q) {
-        const int s = lv.h_fst[q] & 0xffff, t = lv.h_fst[q] >> 16;
+        const int s = lv.h_fst[F.z * g.nfi + q] & 0xffff, t = lv.h_fst[F.z * g.nfi + q] >> 16;
         int w[4] = {0, 0, 0, 0};
         w[F.lA[0]] = N - s - t;
         w[F.lA[1]] = s;
         w[F.lA[2]] = t;
-        serve.push_back({g.base_f + F.fid * g.nfi + lv.h_fcidx[q], (uint32_t)slot_of(F.TA, w[1], w[2], w[3])});
+        serve.push_back({g.base_f + F.fid * g.nfi + lv.h_fcidx[F.z * g.nfi + q],
+                         (uint32_t)slot_of(F.TA, w[1], w[2], w[3])});
       }
     }
     std::sort(serve.begin(), serve.end());
@@ -534,7 +567,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
