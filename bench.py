@@ -273,9 +273,18 @@ def main():
         dom = max(("vol_apply", va_ms, 16, va_n), ("vol_gs", vg_ms, 24, vg_n), key=lambda t: t[1])
         name, tot_ms, bpu, n_launch = dom
         achieved = nvol * bpu * a.steps / (tot_ms * 1e-3) / 1e9
+        kname = "k_gs_items" if name == "vol_gs" else "k_vol_march"
+        traffic, tsrc = None, None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))[kname]
+            traffic, tsrc = tr["bytes"], tr["source"]
+        except Exception:
+            pass
         roof = {"kernel": "k_gs_items (4-colour GS sweep)" if name == "vol_gs" else "k_vol_march (apply)",
                 "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None, "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
+                "frac": achieved / hbm, "traffic": traffic, "traffic_source": tsrc,
+                "algorithmic_bytes_per_launch": nvol * bpu,
+                "peak_source": "measured (MEASURED_PEAKS.json hbm_gbs)",
                 "bytes_per_unknown": bpu, "units_per_launch": nvol * a.steps // max(n_launch, 1),
                 "launches": n_launch, "avg_launch_ms": tot_ms / max(n_launch, 1),
                 "share_of_step": tot_ms / (ms * a.steps),
