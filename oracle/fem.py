@@ -90,13 +90,15 @@ def volume_stencils(mesh, T: int, ijk: np.ndarray, N: int, blended=True) -> np.n
     return out
 
 
-def fem_row(mesh, num: Numbering, gid: int, blended=True) -> dict:
+def fem_row(mesh, num: Numbering, gid: int, blended=True, macros=None) -> dict:
     """Row `gid` of the global FEM matrix (no BC) by node-wise assembly over
-    every fine tet of every macro containing the node: {gid_J: value}."""
+    every fine tet of every macro containing the node: {gid_J: value}.
+    `macros` (optional) lists the candidate macros to search, ascending (a
+    superset of those containing the node); the sum is the same."""
     N = num.N
     lat = lattice_ijk(N)
     row = {}
-    for T in range(mesh.nt):
+    for T in (range(mesh.nt) if macros is None else macros):
         g = num.gids(T, lat)
         hit = np.nonzero(g == gid)[0]
         if len(hit) == 0:

@@ -1,0 +1,167 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (480-macro shell, q = 2 LSQP j = 2, one apply, one residual, one GS
+sweep through the C-ABI), checked on SAMPLED outputs that the oracle computes
+one by one from its own definitions:
+
+* apply / residual at volume nodes: y_I = sum_w P s_w(I) u_(I+w) with the
+  oracle's own LSQP fit of the node's macro;
+* apply at face / edge / vertex nodes: the exact FEM row by node-wise
+  assembly over the macros containing the node;
+* GS at volume nodes >= 5 lattice steps from their macro's boundary: the
+  colour-ordered update (R13/R14) replayed on the node's dependency
+  cone -- a colour-c node reads new values of its lower-colour neighbours,
+  which read theirs, at most 3 levels deep, and the deepest level reads its
+  neighbours 4 steps away -- all volume nodes with their old values (the
+  face class steps before the volume colours do not reach them), so the
+  replay is exact.
+
+Tolerance: |gpu - oracle| <= 1e-12 * sum_w |s_w u_w| per sampled node (the
+row's natural scale; north_star's 1e-12 relative).
+"""
+import functools
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import fem, geometry as G, surrogate as S
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+DIRS = np.array(G.DIRS)
+MC = 7
+
+
+@functools.lru_cache(maxsize=None)
+def case(t, nr, L):
+    import torch
+
+    import paper_1608_06473_b200 as hhg
+    mesh = synth.shell_mesh(0.55, 1.0, t, nr)
+    num = G.Numbering(mesh, 2 ** L)
+    ctx = hhg.Ctx.from_mesh(mesh, L)
+    ctx.fit(2, "lsqp", 2)
+    g = np.arange(num.n_total)
+    u = synth.uniform_pm1(0, g) * num.unknown_mask
+    f = synth.uniform_pm1(1, g) * num.unknown_mask
+    del g
+    du, df = ctx.zeros(L), ctx.zeros(L)
+    ctx.scatter_global(L, torch.from_numpy(u).cuda(), du)
+    ctx.scatter_global(L, torch.from_numpy(f).cuda(), df)
+    dy, dr = ctx.zeros(L), ctx.zeros(L)
+    ctx.apply(L, du, dy)
+    ctx.residual(L, du, df, dr)
+    ctx.gs_sweep(L, du, df, 1)
+    torch.cuda.synchronize()
+    out = {"y": ctx.gather_global(L, dy), "r": ctx.gather_global(L, dr), "ug": ctx.gather_global(L, du)}
+    ctx.close()
+    return mesh, num, u, f, out
+
+
+@functools.lru_cache(maxsize=None)
+def coeffs(t, nr, L, T):
+    mesh = synth.shell_mesh(0.55, 1.0, t, nr)
+    return S.fit_macro(mesh, T, L, 2, "lsqp", 2, blended=True)
+
+
+def sample_volume(rng, N, nt, n, min_dist):
+    out = []
+    while len(out) < n:
+        T = int(rng.integers(nt))
+        i, j, k = (int(x) for x in rng.integers(min_dist, N - min_dist, 3))
+        if i + j + k <= N - min_dist:
+            out.append((T, i, j, k))
+    return out
+
+
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+def test_fullsize_apply_residual_sampled(t, nr, L):
+    mesh, num, u, f, out = case(t, nr, L)
+    N = 2 ** L
+    rng = np.random.default_rng(1234 + L)
+    pts = sample_volume(rng, N, mesh.nt, 96, 1)
+    # include nodes next to every macro face and the farthest corners
+    pts += [(0, 1, 1, 1), (mesh.nt - 1, N - 3, 1, 1), (mesh.nt // 2, 1, N - 3, 1), (7, 1, 1, N - 3)]
+    for T, i, j, k in pts:
+        ijk = np.array([[i, j, k]])
+        sw = S.eval_weights(coeffs(t, nr, L, T), ijk, N, 2)[0]
+        gI = int(num.gids(T, ijk)[0])
+        gn = num.gids(T, ijk + DIRS)
+        un = u[gn]
+        ref = float(np.dot(sw, un))
+        scale = float(np.abs(sw * un).sum())
+        assert abs(out["y"][gI] - ref) <= TOL * scale, (T, i, j, k, out["y"][gI], ref)
+        assert abs(out["r"][gI] - (f[gI] - ref)) <= TOL * (scale + abs(f[gI])), (T, i, j, k)
+
+
+def _containing(mesh, verts):
+    return [T for T in range(mesh.nt) if all(v in set(int(x) for x in mesh.tets[T]) for v in verts)]
+
+
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+def test_fullsize_lower_primitive_rows_sampled(t, nr, L):
+    mesh, num, u, f, out = case(t, nr, L)
+    N = 2 ** L
+    rng = np.random.default_rng(99 + L)
+    gids = []
+    unk_f = np.nonzero(num.unknown_mask[num.base_f:num.base_v])[0] + num.base_f
+    gids += [int(x) for x in rng.choice(unk_f, 12, replace=False)]
+    unk_e = np.nonzero(num.unknown_mask[num.base_e:num.base_f])[0] + num.base_e
+    gids += [int(x) for x in rng.choice(unk_e, 4, replace=False)]
+    unk_v = np.nonzero(num.unknown_mask[:num.base_e])[0]
+    gids += [int(x) for x in rng.choice(unk_v, 2, replace=False)]
+    for g in gids:
+        if g >= num.base_f:
+            verts = num.faces[(g - num.base_f) // num.nfi]
+        elif g >= num.base_e:
+            verts = num.edges[(g - num.base_e) // (N - 1)]
+        else:
+            verts = [g]
+        row = fem.fem_row(mesh, num, g, blended=True, macros=_containing(mesh, [int(v) for v in verts]))
+        cols = np.array(list(row.keys()))
+        vals = np.array([row[c] for c in cols])
+        un = u[cols]
+        ref = float(np.dot(vals, un))
+        scale = float(np.abs(vals * un).sum())
+        assert abs(out["y"][g] - ref) <= TOL * scale, (g, out["y"][g], ref)
+        assert abs(out["r"][g] - (f[g] - ref)) <= TOL * (scale + abs(f[g])), g
+
+
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+def test_fullsize_gs_sweep_sampled(t, nr, L):
+    mesh, num, u, f, out = case(t, nr, L)
+    N = 2 ** L
+    rng = np.random.default_rng(4321 + L)
+    pts = sample_volume(rng, N, mesh.nt, 48, 5)
+    for T, i, j, k in pts:
+        a = coeffs(t, nr, L, T)
+        memo = {}
+
+        def colour(p):
+            return (p[0] + 2 * p[1] + 3 * p[2]) % 4
+
+        def new_value(p):
+            """(value, scale) of volume node p after the volume colour step
+            of its colour (the class steps before it do not touch volume
+            nodes); scale = (|f| + sum_w |s_w v_w|) / |s_mc|."""
+            if p in memo:
+                return memo[p]
+            c = colour(p)
+            ijk = np.array([p])
+            sw = S.eval_weights(a, ijk, N, 2)[0]
+            acc, mag = 0.0, 0.0
+            for w in range(15):
+                if w == MC:
+                    continue
+                q = (p[0] + DIRS[w][0], p[1] + DIRS[w][1], p[2] + DIRS[w][2])
+                v = new_value(q)[0] if colour(q) < c else u[int(num.gids(T, np.array([q]))[0])]
+                acc += sw[w] * v
+                mag += abs(sw[w] * v)
+            gp = int(num.gids(T, ijk)[0])
+            memo[p] = ((f[gp] - acc) / sw[MC], (abs(f[gp]) + mag) / abs(sw[MC]))
+            return memo[p]
+
+        p = (i, j, k)
+        ref, scale = new_value(p)
+        gI = int(num.gids(T, np.array([p]))[0])
+        assert abs(out["ug"][gI] - ref) <= TOL * scale, (T, p, out["ug"][gI], ref)

@@ -63,7 +63,10 @@ def to_local(ctx, L, x):
     return loc
 
 
-CASES = [("tet", 2), ("tet", 3), ("tet", 4), ("tet", 5), ("shell60", 3), ("shell60", 4),
+# ("tet", 7) is BASELINE config 2 at full size (129 nodes per edge, 36 bands of
+# the march kernels); the 480-macro configs at L = 6, 7 are checked on sampled
+# outputs in test_gpu_fullsize.py
+CASES = [("tet", 2), ("tet", 3), ("tet", 4), ("tet", 5), ("tet", 6), ("tet", 7), ("shell60", 3), ("shell60", 4),
          ("shell120", 3), ("shell480", 3)]
 
 
