@@ -304,7 +304,7 @@ def main():
            "profile_ms": prof}
     if rank == 0 and not a.no_extras:
         out["e2e"] = e2e(ctx, L, u, f, y, a, n_owned_total, 1)
-        out["comparisons"] = comparisons(ctx, L, u, y, n_owned) if ws == 1 else None
+        out["comparisons"] = comparisons(ctx, L, u, f, y, n_owned) if ws == 1 else None
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(L, q)
     if rank == 0:
@@ -335,7 +335,7 @@ def e2e(ctx, L, u, f, y, a, n_owned, ws):
             "d2h_bytes_per_step": 2 * nb, "ms_per_step": t * 1e3}
 
 
-def comparisons(ctx, L, u, y, n_owned):
+def comparisons(ctx, L, u, f, y, n_owned):
     """Comparison operators on the same workload (a11/a12): element-wise
     on-the-fly FEM apply and constant-stencil (affine) apply, GLUP/s."""
     import torch
@@ -351,6 +351,23 @@ def comparisons(ctx, L, u, y, n_owned):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / reps
         res[f"{op}_apply"] = {"ms": ms, "glups": n_owned / (ms * 1e-3) / 1e9}
+    # BASELINE config 5 on this GPU's mesh: V(3,3) cycles, levels 2..L, surrogate
+    # GS smoother on every level, 50 CG iterations at L = 2 (u, f ~ U[-1,1]).
+    uu = u.clone()
+    ff = f.clone()
+    ctx.vcycle(L, uu, ff, n_cycles=1)
+    torch.cuda.synchronize()
+    uu.copy_(u)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ncyc = 3
+    e0.record()
+    hist = ctx.vcycle(L, uu, ff, n_cycles=ncyc)
+    e1.record()
+    torch.cuda.synchronize()
+    rates = [hist[i + 1] / hist[i] for i in range(ncyc) if hist[i] > 0]
+    res["vcycle_V33"] = {"ms_per_cycle": e0.elapsed_time(e1) / ncyc, "levels": f"2..{L}",
+                         "residual_history": [float(h) for h in hist],
+                         "reduction_per_cycle": [float(r) for r in rates]}
     return res
 
 
