@@ -236,6 +236,16 @@ static bool force_v1() {
   return v == 1;
 }
 
+// Per-macro k^2 coefficients C_w (coefficient 9 of each weight polynomial),
+// contiguous [T][15], the source of the constant-memory chunks (g_cC).
+static hhg_status ensure_cC(Ctx* c, Level& lv, int op) {
+  if (op != HHG_OP_SURROGATE || lv.d_cC) return HHG_OK;
+  HHG_CK(c, cudaMalloc(&lv.d_cC, (size_t)c->nt_local * 15 * sizeof(double)));
+  HHG_CK(c, cudaMemcpy2DAsync(lv.d_cC, sizeof(double), lv.d_coef10 + 9, 10 * sizeof(double), sizeof(double),
+                              (size_t)c->nt_local * 15, cudaMemcpyDeviceToDevice, c->stream));
+  return HHG_OK;
+}
+
 template <int OP, int MODE>
 static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
@@ -245,11 +255,8 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
     attr = true;
   }
   const int nb = (int)lv.bands.size();
-  if (OP == HHG_OP_SURROGATE && !lv.d_cC) {  // C_w = coefficient 9 of each weight polynomial
-    HHG_CK(c, cudaMalloc(&lv.d_cC, (size_t)c->nt_local * 15 * sizeof(double)));
-    HHG_CK(c, cudaMemcpy2DAsync(lv.d_cC, sizeof(double), lv.d_coef10 + 9, 10 * sizeof(double), sizeof(double),
-                                (size_t)c->nt_local * 15, cudaMemcpyDeviceToDevice, c->stream));
-  }
+  hhg_status st = ensure_cC(c, lv, OP);
+  if (st != HHG_OK) return st;
   ProfScope ps(c, 0);
   for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
     const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
@@ -328,21 +335,30 @@ template <int OP, int MODE, int R>
 static hhg_status launch_pair(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
   const int nb = (int)lv.bands.size();
   const size_t smem = pair_smem_bytes(R, lv.slot_len, lv.N, nb);
-  static bool attr = false;
-  if (!attr) {
+  static int grid = 0;
+  if (grid == 0) {
     HHG_CK(c, cudaFuncSetAttribute(k_vol_pair<OP, MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    112 * 1024));
-    attr = true;
+    int dev = 0, sms = 0, per_sm = 0;
+    HHG_CK(c, cudaGetDevice(&dev));
+    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vol_pair<OP, MODE, R>, kQThreads,
+                                                            pair_smem_bytes(R, 520, 256, 64)));
+    grid = sms * std::max(per_sm, 1);
   }
   if (smem > 112 * 1024) return set_err(c, HHG_ERR_INVALID, "pair march: band too wide for shared memory");
-  int grid = 0;
-  hhg_status st = ensure_schedule(c, lv, (const void*)k_vol_pair<OP, MODE, R>, grid);
+  hhg_status st = ensure_cC(c, lv, OP);
   if (st != HHG_OK) return st;
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
   ProfScope ps(c, 0);
-  k_vol_pair<OP, MODE, R><<<(unsigned)std::min<int64_t>(grid, c->nt_local * nb), kQThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, c->nt_local, lv.d_gs_counter);
-  HHG_LAUNCHED(c);
+  for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
+    const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
+    if (OP == HHG_OP_SURROGATE)
+      HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+    k_vol_pair<OP, MODE, R><<<(unsigned)std::min<int64_t>(grid, nt * nb), kQThreads, smem, c->stream>>>(
+        lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, nt, (int)T0);
+    HHG_LAUNCHED(c);
+  }
   return HHG_OK;
 }
 

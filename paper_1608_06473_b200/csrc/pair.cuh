@@ -35,8 +35,7 @@ struct QSmem {
   uint64_t* iempty; // [kQIQ]
   int* po;          // [N+2]
   int* bk;          // [n_bands] pairs per item
-  int* qitem;       // [kQQ] dynamic item queue (ring); -1 = no more items
-  int* qcount;      // [1] items fetched so far
+  int64_t total;    // items of this launch
   __device__ QSmem(double* smem, int slot_len, int N, int n_bands) {
     ring = smem;
     coef = ring + (size_t)R * 2 * slot_len;
@@ -46,8 +45,6 @@ struct QSmem {
     iempty = ifull + kQIQ;
     po = (int*)(iempty + kQIQ);
     bk = po + (N + 2);
-    qitem = bk + n_bands;
-    qcount = qitem + kQQ;
   }
 };
 
@@ -61,22 +58,18 @@ __host__ __device__ inline size_t pair_smem_bytes(int R, int slot_len, int N, in
 // and share their halo diagonals in L2.  Warp 0 (lane 0) keeps kQFill items
 // fetched ahead of its own position; every warp reads item n from the queue.
 // Returns the item id, -1 past the end, -2 if not fetched yet.
+// Static boustrophedon schedule: item n of CTA c is n*G + c for even n and
+// n*G + G-1-c for odd n (G = grid).  At any time the CTAs work on a window of
+// G consecutive (macro, band) items, so the bands of a macro run concurrently
+// and share their halo diagonals in L2; alternating the direction balances the
+// band lengths (max/mean work 1.06 on the 480-macro L7 shell).  The item id
+// depends only on blockIdx and the loop counter, so the macro index T is
+// uniform and the per-macro k^2 coefficients come from constant memory.
 template <int R>
 __device__ __forceinline__ int queue_item(const QSmem<R>& sm, int n) {
-  if (*(volatile int*)sm.qcount <= n) return -2;
-  return ((volatile int*)sm.qitem)[n & (kQQ - 1)];
-}
-
-template <int R>
-__device__ __forceinline__ void queue_fill(QSmem<R>& sm, int upto, int64_t total, int* __restrict__ counter) {
-  int qc = *(volatile int*)sm.qcount;
-  while (qc < upto) {
-    if (qc > 0 && ((volatile int*)sm.qitem)[(qc - 1) & (kQQ - 1)] < 0) return;  // end reached
-    const int it = atomicAdd(counter, 1);
-    ((volatile int*)sm.qitem)[qc & (kQQ - 1)] = it < total ? it : -1;
-    __threadfence_block();
-    *(volatile int*)sm.qcount = ++qc;
-  }
+  const int G = (int)gridDim.x, cta = (int)blockIdx.x;
+  const int64_t it = (int64_t)n * G + ((n & 1) ? G - 1 - cta : cta);
+  return it < sm.total ? (int)it : -1;
 }
 
 // Issue cursor of one warp (lane 0): the next pair this warp owns (g = warp mod 8).
@@ -152,22 +145,6 @@ __device__ __forceinline__ void qwait(uint64_t* bar, uint32_t parity, PCursor& c
   }
 }
 
-// Item n of this CTA (all lanes of the warp); warp 0 refills the queue.
-template <int R>
-__device__ __forceinline__ int qnext_item(QSmem<R>& sm, int n, int64_t total, int* __restrict__ counter) {
-  const int lane = threadIdx.x & 31;
-  const bool w0 = threadIdx.x < 32;
-  int it;
-  for (;;) {
-    if (w0 && lane == 0) queue_fill(sm, n + kQFill, total, counter);
-    __syncwarp();
-    it = queue_item(sm, n);
-    if (__all_sync(0xffffffffu, it != -2)) break;
-    __nanosleep(64);
-  }
-  return it;
-}
-
 // Column of this thread in band b; inactive lanes get a valid column of the
 // band (their stores are predicated off) so the inner loop is branch-free.
 struct QCol {
@@ -202,14 +179,14 @@ template <int OP, int MODE, int R>
 __global__ void __launch_bounds__(kQThreads, 2)
     k_vol_pair(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, const double* __restrict__ u,
-               const double* __restrict__ f, double* __restrict__ out, int64_t ntl, int* __restrict__ counter) {
+               const double* __restrict__ f, double* __restrict__ out, int64_t ntl, int T0) {
   extern __shared__ __align__(16) double smem[];
   constexpr int kAhead = R - 3;  // pairs a warp issues ahead of its own position
   QSmem<R> sm(smem, slot_len, N, n_bands);
+  sm.total = ntl * n_bands;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int64_t total = ntl * n_bands;
-  const PArgs a{N, S, bands, n_bands, slot_len, coef10, u, nullptr, 0};
+  const PArgs a{N, S, bands, n_bands, slot_len, coef10 + (int64_t)T0 * 150, u + (int64_t)T0 * S, nullptr, 0};
   if (threadIdx.x == 0) {
     for (int s = 0; s < R; ++s) {
       mbar_init(&sm.full[s], 1);
@@ -223,10 +200,6 @@ __global__ void __launch_bounds__(kQThreads, 2)
   }
   for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) sm.po[p] = (int)plane_off(N, p);
   for (int b = threadIdx.x; b < n_bands; b += blockDim.x) sm.bk[b] = (bands[b].kmax + 3) / 2;
-  if (threadIdx.x == 0) {
-    *sm.qcount = 0;
-    queue_fill(sm, kQFill, total, counter);
-  }
   __syncthreads();
 
   PCursor cur;
@@ -240,9 +213,10 @@ __global__ void __launch_bounds__(kQThreads, 2)
 
   int gp = 0;  // global pair number of pair 0 of the current item
   for (int n = 0;; ++n) {
-    const int it = qnext_item(sm, n, total, counter);
+    const int it = queue_item(sm, n);
     if (it < 0) break;
-    const int T = it / n_bands;
+    const int Tl = it / n_bands;  // macro within this launch chunk (uniform)
+    const int T = T0 + Tl;
     const Band b = bands[it - T * n_bands];
     const int e = n & (kQIQ - 1);
     qwait<OP, R>(&sm.ifull[e], (n / kQIQ) & 1, cur, a, sm, gp + kAhead);
@@ -297,7 +271,7 @@ __global__ void __launch_bounds__(kQThreads, 2)
       const double ua[15] = {bc, be, bn, bnw, ms, mse, mw, mc, me, mnw, mn, tse, ts, tw, tc};
       const double ub[15] = {mc, me, mn, mnw, ts, tse, tw, tc, me2, mnw2, mn2, tse2, ts2, tw2, tc2};
       double ra, rb;
-      pnode2<OP>(A, B, cf, (double)k, ua, ub, ra, rb);
+      pnode2<OP>(A, B, g_cC + Tl * 15, (double)k, ua, ub, ra, rb);
       if (k <= q.len) optr[po_k] = (MODE == kModeResid) ? fa - ra : ra;
       if (k + 1 <= q.len) optr[po_k1] = (MODE == kModeResid) ? fb - rb : rb;
       bc = tc; be = me2; bn = mn2; bnw = mnw2;

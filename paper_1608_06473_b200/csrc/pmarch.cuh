@@ -223,7 +223,8 @@ __device__ __forceinline__ double pnode(const double (&A)[15], const double (&B)
   return (acc[0] + acc[1]) + acc[2];
 }
 
-// Two nodes k, k+1 of one column.  The weight polynomial is expanded instead
+// Two nodes k, k+1 of one column (cf = the 15 per-macro k^2 coefficients C_w).
+// The weight polynomial is expanded instead
 // of evaluated by Horner per weight:
 //   sum_w s_w(k) u_w = sum_w A_w u_w + k sum_w B_w u_w + k^2 sum_w C_w u_w,
 // six independent accumulation chains (three per node) instead of fifteen
@@ -237,7 +238,7 @@ __device__ __forceinline__ void pnode2(const double (&A)[15], const double (&B)[
     double xa = 0.0, ya = 0.0, za = 0.0, xb = 0.0, yb = 0.0, zb = 0.0;
 #pragma unroll
     for (int w = 0; w < 15; ++w) {
-      const double c = cf[w * 10 + 9];
+      const double c = cf[w];
       xa = fma(A[w], ua[w], xa);
       xb = fma(A[w], ub[w], xb);
       ya = fma(B[w], ua[w], ya);
@@ -393,8 +394,10 @@ __global__ void __launch_bounds__(kPThreads, 2)
             const double* Pk2 = sptr(k + 2);
             const double tc2 = Pk2[q.o_c], tw2 = Pk2[q.o_w], ts2 = Pk2[q.o_s], tse2 = Pk2[q.o_se];
             const double ub[15] = {mc, me, mn, mnw, ts, tse, tw, tc, me2, mnw2, mn2, tse2, ts2, tw2, tc2};
-            double ra, rb;
-            pnode2<OP>(A, B, cf, (double)k, ua, ub, ra, rb);
+            double ra, rb, cw[15];
+#pragma unroll
+            for (int w = 0; w < 15; ++w) cw[w] = cf[w * 10 + 9];
+            pnode2<OP>(A, B, cw, (double)k, ua, ub, ra, rb);
             optr[sm.po[k]] = (MODE == kModeResid) ? fa - ra : ra;
             optr[sm.po[k + 1]] = (MODE == kModeResid) ? fb - rb : rb;
             bc = tc; be = me2; bn = mn2; bnw = mnw2;
