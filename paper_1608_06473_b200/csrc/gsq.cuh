@@ -224,14 +224,6 @@ __device__ __forceinline__ void gs_wait(uint64_t* bar, uint32_t parity, GCursor&
   }
 }
 
-#ifdef HHG_GS_PROF
-__device__ unsigned long long g_gsprof[8];  // [0] data waits, [1] barrier, [2] item waits, [3] total, [4] quads
-#define GPROF_T0 long long _t0 = clock64();
-#define GPROF_ADD(i) if (threadIdx.x == 0) atomicAdd(&g_gsprof[i], (unsigned long long)(clock64() - _t0));
-#else
-#define GPROF_T0
-#define GPROF_ADD(i)
-#endif
 
 template <int OP>
 __global__ void __launch_bounds__(kGThreads, 2)

@@ -27,6 +27,16 @@
 
 namespace hhg {
 
+// Optional cycle accounting of the GS kernels (build with -DHHG_GS_PROF; tools/gsprof.py).
+#ifdef HHG_GS_PROF
+__device__ unsigned long long g_gsprof[8];
+#define GPROF_T0 long long _t0 = clock64();
+#define GPROF_ADD(i) if (threadIdx.x == 0) atomicAdd(&g_gsprof[i], (unsigned long long)(clock64() - _t0));
+#else
+#define GPROF_T0
+#define GPROF_ADD(i)
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -38,6 +48,10 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -60,26 +74,28 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
-// Issue the bulk copy of plane p's band range into ring slot p % kRing
+// Issue the bulk copy of plane p's band range into ring slot p % RING
 // (po = plane offset table in shared memory).
+template <int RING = kRing>
 __device__ __forceinline__ void issue_plane(const double* ub, const int* po, int p, const Band& b, double* ring,
                                             int slot_len, uint64_t* bars) {
   const int g0 = po[p] + b.c_lo;
   const int a0 = g0 & ~1;
   const int a1 = (g0 + b.ncols + 1) & ~1;
   const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
-  const int s = p & (kRing - 1);
+  const int s = p % RING;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   mbar_expect_tx(&bars[s], bytes);
   tma_load_1d(ring + s * slot_len, ub + a0, bytes, &bars[s]);
 }
 
 // Warp 0 issues planes [from, to] in parallel, one lane per plane (to - from < 32).
+template <int RING = kRing>
 __device__ __forceinline__ void issue_planes(const double* ub, const int* po, int from, int to, const Band& b,
                                              double* ring, int slot_len, uint64_t* bars) {
   if (threadIdx.x < 32) {
     const int p = from + (int)threadIdx.x;
-    if (p <= to) issue_plane(ub, po, p, b, ring, slot_len, bars);
+    if (p <= to) issue_plane<RING>(ub, po, p, b, ring, slot_len, bars);
   }
 }
 
@@ -94,22 +110,23 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
-// Shared-memory carve-up common to the march kernels.
+// Shared-memory carve-up common to the march kernels (RING plane slots).
+template <int RING = kRing>
 struct MarchSmem {
-  double* ring;     // [kRing][slot_len]
-  uint64_t* bars;   // [kRing]
+  double* ring;     // [RING][slot_len]
+  uint64_t* bars;   // [RING]
   double* Cw;       // [16] k^2 coefficients of the 15 weights (per macro)
   int* po;          // [N+2] plane offsets
   __device__ MarchSmem(double* smem, int slot_len) {
     ring = smem;
-    bars = (uint64_t*)(smem + kRing * slot_len);
-    Cw = (double*)(bars + kRing);
+    bars = (uint64_t*)(smem + RING * slot_len);
+    Cw = (double*)(bars + RING);
     po = (int*)(Cw + 16);
   }
 };
 
-__host__ __device__ inline size_t march_smem_bytes(int slot_len, int N) {
-  return (size_t)kRing * slot_len * 8 + kRing * 8 + 16 * 8 + (size_t)(N + 2) * 4;
+__host__ __device__ inline size_t march_smem_bytes(int slot_len, int N, int ring = kRing) {
+  return (size_t)ring * slot_len * 8 + ring * 8 + 16 * 8 + (size_t)(N + 2) * 4;
 }
 
 struct Column {
@@ -164,7 +181,7 @@ __device__ __forceinline__ void column_coeffs(const double* coef10, const double
   }
 }
 
-__device__ __forceinline__ void march_prologue(MarchSmem& sm, const Band& b, int N, const double* coef10,
+__device__ __forceinline__ void march_prologue(MarchSmem<>& sm, const Band& b, int N, const double* coef10,
                                                int64_t T, int op) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < kRing; ++s) mbar_init(&sm.bars[s], 1);
@@ -191,7 +208,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
                 const double* __restrict__ coef10, const double* __restrict__ cons,
                 const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out, int T0) {
   extern __shared__ __align__(16) double smem[];
-  MarchSmem sm(smem, slot_len);
+  MarchSmem<> sm(smem, slot_len);
   const int Tl = blockIdx.x / n_bands;  // macro within the launch chunk (uniform)
   const int64_t T = T0 + Tl;
   const Band b = bands[blockIdx.x - Tl * n_bands];
@@ -306,33 +323,38 @@ struct ProgGate {
   }
 };
 
-template <int OP, class Gate = NoGate>
-__device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int N, const Band& b, const Column& q,
+template <int OP, int RING = kRing, class Gate = NoGate>
+__device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len, int N, const Band& b, const Column& q,
                                                const double (&A)[15], const double (&B)[15], int colour,
                                                double* __restrict__ ub, const double* __restrict__ fb,
                                                double* __restrict__ wb, const Gate& gate = Gate()) {
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kRing; ++s) mbar_init(&sm.bars[s], 1);
+    for (int s = 0; s < RING; ++s) mbar_init(&sm.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   // colour(i,j,k) = (d + j + 3k) mod 4 == colour  <=>  k == 3 (colour - d - j) mod 4
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
   const int last_plane = b.kmax + 1;
-  int next_issue = min(kRing, last_plane + 1);
+  int next_issue = min(RING, last_plane + 1);
   if (threadIdx.x < 32) gate.wait(next_issue - 1);
-  issue_planes(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
+  issue_planes<RING>(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
   const int clo = b.c_lo;
   auto sptr = [&](int p) -> const double* {
-    return sm.ring + (p & (kRing - 1)) * slot_len + ((sm.po[p] + clo) & 1);
+    return sm.ring + (p % RING) * slot_len + ((sm.po[p] + clo) & 1);
   };
   auto wait_plane = [&](int p) {
-    if (p <= last_plane) mbar_wait(&sm.bars[p & (kRing - 1)], (p / kRing) & 1);
+    if (p <= last_plane) mbar_wait(&sm.bars[p % RING], (p / RING) & 1);
   };
   const int nsteps = (b.kmax + 4) / 4;
   double f_next = 0.0;
   if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
-  wait_plane(0);
+  {
+    GPROF_T0
+    wait_plane(0);
+    wait_plane(1);
+    GPROF_ADD(2)
+  }
   for (int s = 0; s < nsteps; ++s) {
     // planes 4s+1 .. 4s+4 become needed at step s (4s-1, 4s were waited before)
     wait_plane(4 * s + 1);
@@ -376,20 +398,137 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem& sm, int slot_len, int 
       wb[sm.po[k]] = (fv - r) * rinv;
     }
     // every 3 steps: all warps done with planes <= 4s+2 (next step reads >= 4s+3);
-    // refill up to plane 4s+18 (the following 3 steps need <= 4s+16).
+    // refill up to plane 4s+2+RING (the following 3 steps need <= 4s+16; with
+    // RING = 24 the planes of the step after the next refill are already in flight).
     if (s % 3 == 2 || s == nsteps - 1) {
       __syncthreads();
       gate.publish(colour * 1024 + min(4 * s + 4, last_plane + 1));
-      const int to = min(4 * s + 2 + kRing, last_plane);
+      const int to = min(4 * s + 2 + RING, last_plane);
       if (to >= next_issue && threadIdx.x < 32) gate.wait(to);
-      issue_planes(ub, sm.po, next_issue, to, b, sm.ring, slot_len, sm.bars);
+      issue_planes<RING>(ub, sm.po, next_issue, to, b, sm.ring, slot_len, sm.bars);
       next_issue = max(next_issue, to + 1);
     }
   }
 }
 
-template <int OP>
-__device__ __forceinline__ void band_setup(MarchSmem& sm, int N, const Band& b, int64_t T,
+// Same colour pass with QUAD mbarriers: the ring of RING planes is RING/4
+// slots of 4 planes whose bulk copies complete on one barrier (arrival count
+// 4: one arrive.expect_tx per plane, plain arrives past the last plane), so a
+// thread waits once per step (4 planes) instead of four times.
+template <int OP, int RING, class Gate = NoGate>
+__device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_len, int N, const Band& b,
+                                                 const Column& q, const double (&A)[15], const double (&B)[15],
+                                                 int colour, double* __restrict__ ub, const double* __restrict__ fb,
+                                                 double* __restrict__ wb, const Gate& gate = Gate()) {
+  constexpr int NQ = RING / 4;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NQ; ++s) mbar_init(&sm.bars[s], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
+  const int last_plane = b.kmax + 1;
+  const int last_quad = last_plane / 4;
+  const int clo = b.c_lo;
+  // warp 0: issue quads [q0, q1] (lane = plane within the group)
+  auto issue_quads = [&](int q0, int q1) {
+    if (threadIdx.x < 32 && q1 >= q0) {
+      gate.wait(min(4 * q1 + 3, last_plane));
+      for (int p = 4 * q0 + (int)threadIdx.x; p <= 4 * q1 + 3; p += 32) {
+        uint64_t* bar = &sm.bars[(p >> 2) % NQ];
+        if (p <= last_plane) {
+          const int g0 = sm.po[p] + b.c_lo;
+          const int a0 = g0 & ~1;
+          const int a1 = (g0 + b.ncols + 1) & ~1;
+          const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
+          mbar_expect_tx(bar, bytes);
+          tma_load_1d(sm.ring + (p % RING) * slot_len, ub + a0, bytes, bar);
+        } else {
+          mbar_arrive(bar);
+        }
+      }
+    }
+  };
+  int next_quad = min(NQ, last_quad + 1);
+  issue_quads(0, next_quad - 1);
+  auto sptr = [&](int p) -> const double* {
+    return sm.ring + (p % RING) * slot_len + ((sm.po[p] + clo) & 1);
+  };
+  int waited = -1;
+  auto wait_quads = [&](int qq) {
+    qq = min(qq, last_quad);
+    for (; waited < qq;) {
+      ++waited;
+      mbar_wait(&sm.bars[waited % NQ], (waited / NQ) & 1);
+    }
+  };
+  const int nsteps = (b.kmax + 4) / 4;
+  double f_next = 0.0;
+  if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
+  for (int s = 0; s < nsteps; ++s) {
+    {
+      GPROF_T0
+      wait_quads(s + 1);  // planes 4s-1 .. 4s+4
+      GPROF_ADD(5)
+    }
+    GPROF_T0
+    const int k = 4 * s + delta;
+    const double fv = f_next;
+    if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
+    if (q.active && k >= 1 && k <= q.len) {
+      const double kd = (double)k;
+      const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(sm.Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
+      const double rinv = rcp_nr(smc);
+      const double* Pb = sptr(k - 1);
+      const double* Pm = sptr(k);
+      const double* Pt = sptr(k + 1);
+      const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
+                             Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
+                             Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
+      double r;
+      if (OP == HHG_OP_SURROGATE) {
+        double x = 0.0, y = 0.0, z = 0.0;
+#pragma unroll
+        for (int w = 0; w < 15; ++w) {
+          if (w == kMC) continue;
+          x = fma(A[w], uu[w], x);
+          y = fma(B[w], uu[w], y);
+          z = fma(sm.Cw[w], uu[w], z);
+        }
+        r = fma(fma(z, kd, y), kd, x);
+      } else {
+        double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int w = 0; w < 15; ++w) {
+          if (w == kMC) continue;
+          acc[w % 3] = fma(A[w], uu[w], acc[w % 3]);
+        }
+        r = (acc[0] + acc[1]) + acc[2];
+      }
+      wb[sm.po[k]] = (fv - r) * rinv;
+    }
+    GPROF_ADD(6)
+    // every 3 steps: all warps done with quads <= s-1 (the next step reads planes >= 4s+3);
+    // refill them: quads up to s-1+NQ (the next three steps need quads <= s+4).
+    if (s % 3 == 2 || s == nsteps - 1) {
+      GPROF_T0
+      __syncthreads();
+      GPROF_ADD(7)
+      gate.publish(colour * 1024 + min(4 * s + 4, last_plane + 1));
+      const int to = min(s - 1 + NQ, last_quad);
+      {
+        GPROF_T0
+        issue_quads(next_quad, to);
+        GPROF_ADD(2)
+      }
+      next_quad = max(next_quad, to + 1);
+    }
+  }
+  wait_quads(last_quad);  // every issued quad is consumed before the barriers are re-initialised
+}
+
+template <int OP, int RING = kRing>
+__device__ __forceinline__ void band_setup(MarchSmem<RING>& sm, int N, const Band& b, int64_t T,
                                            const double* __restrict__ coef10, const double* __restrict__ cons,
                                            Column& q, double (&A)[15], double (&B)[15]) {
   q = make_column(b, N);
@@ -406,7 +545,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
                const double* __restrict__ coef10, const double* __restrict__ cons, int colour,
                double* __restrict__ u, const double* __restrict__ f) {
   extern __shared__ __align__(16) double smem[];
-  MarchSmem sm(smem, slot_len);
+  MarchSmem<> sm(smem, slot_len);
   const int64_t T = blockIdx.x / n_bands;
   const Band b = bands[blockIdx.x - T * n_bands];
   Column q;
@@ -428,17 +567,20 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // running yet; every other running item's neighbours run too => no deadlock
 // while the grid has more CTAs than a macro has bands.
 // ---------------------------------------------------------------------------
-template <int OP, int NT>
+template <int OP, int NT, int RING>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
                const double* __restrict__ f, int64_t ntl, int G, int* __restrict__ counter,
                int* __restrict__ flags, int epoch) {
   extern __shared__ __align__(16) double smem[];
-  MarchSmem sm(smem, slot_len);
+  MarchSmem<RING> sm(smem, slot_len);
   __shared__ int s_item;
   (void)G;
   const int64_t total = ntl * n_bands;
+#ifdef HHG_GS_PROF
+  if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)(-clock64()));
+#endif
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -450,8 +592,13 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const Band b = bands[band];
     Column q;
     double A[15], B[15];
-    band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
+    {
+      GPROF_T0
+      band_setup<OP, RING>(sm, N, b, T, coef10, cons, q, A, B);
+      GPROF_ADD(4)
+    }
     for (int colour = 0; colour < 4; ++colour) {
+      GPROF_T0
       if (threadIdx.x == 0 && colour > 0) {
         for (int bb = band - 1; bb <= band + 1; bb += 2) {
           if (bb < 0 || bb >= n_bands) continue;
@@ -459,15 +606,32 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           while (*fl != epoch) __nanosleep(32);
         }
         __threadfence();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
       }
       __syncthreads();
-      gs_colour_pass<OP>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
-      __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
+      // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
+      // neighbours' generic global writes before their async-proxy reads
+      if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
+      GPROF_ADD(0)
+      {
+        GPROF_T0
+        if (RING % 8 == 0 && RING >= 24)
+          gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
+                                     u + T * S + q.c);
+        else
+          gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
+        __syncthreads();
+        GPROF_ADD(1)
+      }
+      // bar.sync orders every thread's stores before thread 0's gpu-scope fence (cumulative)
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
+      }
     }
   }
+#ifdef HHG_GS_PROF
+  if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)clock64());
+#endif
 }
 
 // Same items and colour passes, but with PLANE-level dependencies: pass c of
@@ -475,14 +639,14 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 // to plane p+1 (each band publishes its progress at every ring refill), so a
 // pass overlaps the tail of its neighbours' previous pass instead of waiting
 // for their completion.  prog[T][b] = epoch * 8192 + pass * 1024 + planes done.
-template <int OP, int NT>
+template <int OP, int NT, int RING>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items_p(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                  const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
                  const double* __restrict__ f, int64_t ntl, int* __restrict__ counter, int* __restrict__ prog,
                  int epoch) {
   extern __shared__ __align__(16) double smem[];
-  MarchSmem sm(smem, slot_len);
+  MarchSmem<RING> sm(smem, slot_len);
   __shared__ int s_item;
   const int64_t total = ntl * n_bands;
   for (;;) {
@@ -496,14 +660,15 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const Band b = bands[band];
     Column q;
     double A[15], B[15];
-    band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
+    band_setup<OP, RING>(sm, N, b, T, coef10, cons, q, A, B);
     int* row = prog + T * n_bands;
     ProgGate gate{row + band, band > 0 ? row + band - 1 : nullptr, band + 1 < n_bands ? row + band + 1 : nullptr,
                   epoch * 8192, 0};
     for (int colour = 0; colour < 4; ++colour) {
       gate.colour = colour;
       if (colour > 0 && threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
-      gs_colour_pass<OP>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c, gate);
+      gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c,
+                               gate);
       __syncthreads();
       gate.publish((colour + 1) * 1024);
     }

@@ -388,22 +388,22 @@ static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, cons
   return HHG_OK;
 }
 
-template <int OP, int NT>
+template <int OP, int NT, int RING>
 static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double* f) {
   const bool narrow = NT == kNarrowThreads;
   const std::vector<Band>& bands = narrow ? lv.bands_s : lv.bands;
   const Band* d_bands = narrow ? lv.d_bands_s : lv.d_bands;
   int* flags = narrow ? lv.d_gs_flags_s : lv.d_gs_flags;
   const int slot_len = narrow ? lv.slot_len_s : lv.slot_len;
-  const size_t smem = march_smem_bytes(slot_len, lv.N);
+  const size_t smem = march_smem_bytes(slot_len, lv.N, RING);
   static int grid = 0;
   if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
     int dev = 0, sms = 0, per_sm = 0;
     HHG_CK(c, cudaGetDevice(&dev));
     HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT>, NT,
-                                                            march_smem_bytes(narrow ? 400 : 520, 256)));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT, RING>, NT,
+                                                            march_smem_bytes(narrow ? 400 : 520, 256, RING)));
     grid = sms * std::max(per_sm, 1);
   }
   const int nb = (int)bands.size();
@@ -433,15 +433,15 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
   if (gated) {
     static bool attr = false;
     if (!attr) {
-      HHG_CK(c, cudaFuncSetAttribute(k_gs_items_p<OP, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      HHG_CK(c, cudaFuncSetAttribute(k_gs_items_p<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      110 * 1024));
       attr = true;
     }
-    k_gs_items_p<OP, NT><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+    k_gs_items_p<OP, NT, RING><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
         lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter, flags,
         lv.gs_epoch);
   } else {
-    k_gs_items<OP, NT><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+    k_gs_items<OP, NT, RING><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
         lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G, lv.d_gs_counter, flags,
         lv.gs_epoch);
   }
@@ -456,8 +456,14 @@ static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f)
     const char* e = getenv("HHG_GS_CTA");
     nt = (e && atoi(e) == 128) ? 128 : 256;
   }
-  if (nt == 128 && !lv.bands_s.empty()) return launch_gs_items_nt<OP, kNarrowThreads>(c, lv, u, f);
-  return launch_gs_items_nt<OP, kMarchThreads>(c, lv, u, f);
+  static int ring = -1;  // HHG_GS_RING=16 -> the apply kernels' ring depth
+  if (ring < 0) {
+    const char* e = getenv("HHG_GS_RING");
+    ring = (e && atoi(e) == 16) ? 16 : 24;
+  }
+  if (nt == 128 && !lv.bands_s.empty()) return launch_gs_items_nt<OP, kNarrowThreads, 24>(c, lv, u, f);
+  if (ring == 16) return launch_gs_items_nt<OP, kMarchThreads, 16>(c, lv, u, f);
+  return launch_gs_items_nt<OP, kMarchThreads, 24>(c, lv, u, f);
 }
 
 // Whole volume GS sweep as one continuously pipelined persistent launch (gsq.cuh).
