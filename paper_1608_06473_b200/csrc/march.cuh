@@ -84,7 +84,6 @@ __device__ __forceinline__ void issue_plane(const double* ub, const int* po, int
   const int a1 = (g0 + b.ncols + 1) & ~1;
   const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
   const int s = p % RING;
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   mbar_expect_tx(&bars[s], bytes);
   tma_load_1d(ring + s * slot_len, ub + a0, bytes, &bars[s]);
 }
@@ -213,14 +212,15 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   const int64_t T = T0 + Tl;
   const Band b = bands[blockIdx.x - Tl * n_bands];
   const double* ub = u + T * S;
-  const Column q = make_column(b, N);
-  double A[15], B[15];
-  column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
+  // barriers + plane offsets, then the first kRing planes are put in flight
+  // BEFORE the column coefficients are computed (their HBM latency overlaps it)
   march_prologue(sm, b, N, coef10, T, OP);
-
   const int last_plane = b.kmax + 1;
   int next_issue = min(kRing, last_plane + 1);  // uniform across the CTA
   issue_planes(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
+  const Column q = make_column(b, N);
+  double A[15], B[15];
+  column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
 
   const int clo = b.c_lo;
   auto sptr = [&](int p, int pof) -> const double* {
@@ -238,8 +238,13 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   }
   double* const optr = out + T * S + q.c;
   const double* const fptr = f + T * S + q.c;
+  // residual: f of node k+1 is loaded one step ahead (its latency hides behind a step)
+  double fnext = 0.0;
+  if (MODE == kModeResid && q.active && 1 <= q.len) fnext = __ldg(fptr + po1);
   for (int k = 1; k <= b.kmax; ++k) {
     const int po2 = sm.po[k + 1];
+    const double fv = fnext;
+    if (MODE == kModeResid && q.active && k + 1 <= q.len) fnext = __ldg(fptr + po2);
     mbar_wait(&sm.bars[(k + 1) & (kRing - 1)], ((k + 1) / kRing) & 1);
     if (q.active && k <= q.len) {
       const double* Pk = sptr(k, po1);
@@ -247,8 +252,6 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
       const double me = Pk[q.o_e], mn = Pk[q.o_n], mnw = Pk[q.o_nw];
       const double tc = Pk1[q.o_c], tw = Pk1[q.o_w], ts = Pk1[q.o_s], tse = Pk1[q.o_se];
       const double uu[15] = {bc, be, bn, bnw, ms, mse, mw, mc, me, mnw, mn, tse, ts, tw, tc};
-      double fv = 0.0;
-      if (MODE == kModeResid) fv = __ldg(fptr + po1);
       double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       if (OP == HHG_OP_SURROGATE) {
         const double kd = (double)k;
