@@ -43,6 +43,9 @@ def parse():
     p.add_argument("--q", type=int, default=2)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-extras", action="store_true")
+    p.add_argument("--transport", default="nccl", choices=["nccl", "host"],
+                   help="multi-rank exchange: NCCL (production) or host/gloo (functional check of the "
+                        "multi-rank path with several ranks sharing one GPU)")
     return p.parse_args()
 
 
@@ -181,12 +184,20 @@ def main():
     import synth
 
     ws, rank, local = dist_env()
+    host_tr = a.transport == "host"
+    if host_tr:
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if host_tr:
+            dist.init_process_group("gloo")
+            hhg.set_torch_transport()
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    rdev = torch.device("cpu") if host_tr else dev  # device of the reduction tensors
     stream = torch.cuda.current_stream(dev)
     L, q = a.L, a.q
     # weak scaling (BASELINE config 4): ~480 macros per GPU --
@@ -199,11 +210,14 @@ def main():
     if ws > 1:
         # one process per GPU; the library's ghost exchange runs over NCCL
         # (contiguous macro ranges = radial layers / surface patches per rank)
-        nid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(nid, src=0)
         owner = (np.arange(mesh.nt) * ws) // mesh.nt
-        ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream, rank=rank, nranks=ws, owner=owner,
-                                nccl_id=nid[0])
+        if host_tr:
+            ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream, rank=rank, nranks=ws, owner=owner)
+        else:
+            nid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(nid, src=0)
+            ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream, rank=rank, nranks=ws, owner=owner,
+                                    nccl_id=nid[0])
     else:
         ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream)
     ctx.fit(q, "lsqp", 2)
@@ -212,7 +226,7 @@ def main():
     n_local, n_owned, n_global = ctx.layout(L)
     n_owned_total = n_owned
     if ws > 1:
-        tt = torch.tensor([float(n_owned)], device=dev)
+        tt = torch.tensor([float(n_owned)], device=rdev)
         dist.all_reduce(tt)
         n_owned_total = int(tt.item())
     # inputs: seeded U[-1,1] on canonical ids (generated on the host once)
@@ -252,7 +266,7 @@ def main():
     launches = ctx.kernel_launches - launches0
     ms = ev0.elapsed_time(ev1) / a.steps
     if dist:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device=rdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     lups_step = 2 * n_owned_total
@@ -262,7 +276,8 @@ def main():
     hbm = pk.get("hbm_gbs", 6650.0)
     # dominant kernel: volume kernels; algorithmic bytes per volume unknown:
     # apply 16 B (u in, y out), GS 24 B (u in, f in, u out) -- SURVEY 8(d)
-    nvol = ctx.nt * ((2 ** L - 1) * (2 ** L - 2) * (2 ** L - 3) // 6)
+    nt_local = ctx.plan_info(L)["local_macros"] if ws > 1 else ctx.nt  # this rank's macros (timed kernels)
+    nvol = nt_local * ((2 ** L - 1) * (2 ** L - 2) * (2 ** L - 3) // 6)
     va_ms, va_n = prof["vol_apply"]
     vg_ms, vg_n = prof["vol_gs"]
     roof = None
@@ -295,7 +310,11 @@ def main():
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"shell t={t_ref} n_r={nr_ref} ({mesh.nt} macros) L={L} q={q} LSQP j=2, "
                                   f"apply + 1 GS sweep", "unknowns": n_owned_total,
-                      "macros_per_gpu": mesh.nt // ws, "parallelism": f"macro partition over {ws} GPUs, NCCL ghost exchange" if ws > 1 else "1 GPU",
+                      "macros_per_gpu": mesh.nt // ws,
+                      "parallelism": (f"macro partition over {ws} ranks, "
+                                      + ("host (gloo) ghost exchange, ranks sharing a GPU: functional check, "
+                                         "not a performance number" if host_tr else "NCCL ghost exchange"))
+                      if ws > 1 else "1 GPU",
                       "l2": "inputs larger than L2 (1 vector = %.2f GB)" % (n_local * 8 / 1e9),
                       "setup_s": round(t_setup, 2)},
            "gpu_launches": launches,
