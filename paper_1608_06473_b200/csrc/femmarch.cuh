@@ -1,0 +1,174 @@
+// On-the-fly FEM apply / residual (the paper's comparison operator,
+// PAPER.md:385-394, 1102-1122): every interior node's 15 stencil weights are
+// assembled from the local stiffness matrices of its 24 incident fine tets,
+// with the fine-tet vertices at their blended positions, on every call
+// (nothing stored).  Column-march structure of march.cuh: thread = lattice
+// column, planes of u through a TMA ring.  What the v1 node-wise kernel
+// recomputed per tet is shared here: every blended node position is computed
+// once per call (plane by plane into a 4-plane shared-memory ring, by the
+// threads of the band) and the 24 incident tets of an interior node come from
+// a fixed direction table, so a node costs 24 x (gradients, 1 division, 4
+// dot products) ~ 1.6 kflop.  Same arithmetic as the oracle's definition
+// (blended vertices, K_T = |T| grad(l_a).grad(l_b)), summation order differs.
+#pragma once
+#include "fem_device.cuh"
+#include "march.cuh"
+
+namespace hhg {
+
+constexpr int kFRing = 8;  // u plane slots
+
+// The 24 fine tets incident to an interior lattice node, as the directions
+// (HHG_DIRS_INIT order; 7 = the node) of their 4 vertices -- fem_partial's
+// enumeration (6 Kuhn paths x the node's position m = t % 4 on the path).
+__device__ constexpr int kFemTet[24][4] = {{7, 8, 10, 14}, {6, 7, 9, 13},  {4, 5, 7, 12},  {0, 1, 2, 7},   {7, 8, 11, 14},
+                                {6, 7, 12, 13}, {3, 2, 7, 9},   {0, 1, 5, 7},   {7, 9, 10, 14}, {5, 7, 8, 11},
+                                {4, 6, 7, 12},  {0, 3, 2, 7},   {7, 9, 13, 14}, {5, 7, 12, 11}, {1, 2, 7, 8},
+                                {0, 3, 6, 7},   {7, 12, 11, 14}, {2, 7, 8, 10},  {3, 6, 7, 9},   {0, 4, 5, 7},
+                                {7, 12, 13, 14}, {2, 7, 9, 10},  {1, 5, 7, 8},   {0, 4, 6, 7}};
+
+struct FemSmem {
+  double* ring;   // [kFRing][slot_len] u planes
+  double* pos;    // [4][3][slot_len] node positions (x, y, z planes) of lattice planes k mod 4
+  uint64_t* bars; // [kFRing]
+  int* po;        // [N+2]
+  __device__ FemSmem(double* smem, int slot_len, int N) {
+    ring = smem;
+    pos = ring + (size_t)kFRing * slot_len;
+    bars = (uint64_t*)(pos + (size_t)12 * slot_len);
+    po = (int*)(bars + kFRing);
+  }
+};
+
+__host__ __device__ inline size_t fem_smem_bytes(int slot_len, int N) {
+  return (size_t)kFRing * slot_len * 8 + (size_t)12 * slot_len * 8 + kFRing * 8 + (size_t)(N + 2) * 4;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kMarchThreads, 2)
+    k_vol_fem(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
+              const double* __restrict__ geo_all, bool blended, const double* __restrict__ u,
+              const double* __restrict__ f, double* __restrict__ out) {
+  extern __shared__ __align__(16) double smem[];
+  FemSmem sm(smem, slot_len, N);
+  const int64_t T = blockIdx.x / n_bands;
+  const Band b = bands[blockIdx.x - T * n_bands];
+  const double* ub = u + T * S;
+  const double* geo = geo_all + T * 16;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kFRing; ++s) mbar_init(&sm.bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) sm.po[p] = (int)plane_off(N, p);
+  __syncthreads();
+
+  const int last_plane = b.kmax + 1;
+  int next_issue = min(kFRing - 1, last_plane + 1);
+  issue_planes<kFRing>(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
+  const Column q = make_column(b, N);
+  const int clo = b.c_lo;
+  // lattice columns of the ring range this thread computes positions for
+  int pc_i[2], pc_j[2];
+  for (int r = 0; r < 2; ++r) {
+    const int c = clo + (int)threadIdx.x + r * kMarchThreads;
+    int d = (int)((sqrt(8.0 * (double)c + 1.0) - 1.0) * 0.5);
+    while ((d + 1) * (d + 2) / 2 <= c) ++d;
+    while (d * (d + 1) / 2 > c) --d;
+    pc_j[r] = c - d * (d + 1) / 2;
+    pc_i[r] = d - pc_j[r];
+  }
+  auto positions = [&](int k) {  // plane k -> pos slot k & 3
+    double* P = sm.pos + (size_t)(k & 3) * 3 * slot_len;
+    for (int r = 0; r < 2; ++r) {
+      const int o = (int)threadIdx.x + r * kMarchThreads;
+      if (o >= b.ncols + 1) continue;
+      const int i = pc_i[r], j = pc_j[r];
+      if (i < 0 || j < 0 || i + j + k > N) continue;
+      double x[3];
+      node_xyz(geo, N, i, j, k, blended, x);
+      P[o] = x[0];
+      P[slot_len + o] = x[1];
+      P[2 * slot_len + o] = x[2];
+    }
+  };
+  positions(0);
+  positions(1);
+  auto sptr = [&](int p) -> const double* {
+    return sm.ring + (p % kFRing) * slot_len + ((sm.po[p] + clo) & 1);
+  };
+  double* const optr = out + T * S + q.c;
+  const double* const fptr = f + T * S + q.c;
+  for (int k = 1; k <= b.kmax; ++k) {
+    positions(k + 1);
+    __syncthreads();  // positions of k+1 visible; every thread is done with step k-1 (u plane k-2 free)
+    if (k + 6 <= last_plane && k + 6 >= next_issue) {
+      issue_planes<kFRing>(ub, sm.po, k + 6, k + 6, b, sm.ring, slot_len, sm.bars);
+      next_issue = k + 7;
+    }
+    mbar_wait(&sm.bars[(k + 1) % kFRing], ((k + 1) / kFRing) & 1);
+    if (k == 1) mbar_wait(&sm.bars[0], 0), mbar_wait(&sm.bars[1], 0);
+    if (!(q.active && k <= q.len)) continue;
+    double fv = 0.0;
+    if (MODE == kModeResid) fv = __ldg(fptr + sm.po[k]);
+    const double* Pl0 = sm.pos + (size_t)((k - 1) & 3) * 3 * slot_len;
+    const double* Pl1 = sm.pos + (size_t)(k & 3) * 3 * slot_len;
+    const double* Pl2 = sm.pos + (size_t)((k + 1) & 3) * 3 * slot_len;
+    const double* Ul0 = sptr(k - 1);
+    const double* Ul1 = sptr(k);
+    const double* Ul2 = sptr(k + 1);
+    // y_I = sum over the 24 incident tets T of sum_a |T| grad(l_I).grad(l_a) u_a
+    double acc = 0.0;
+    // ring offsets of the 15 directions (7 distinct columns)
+    const int ocol[15] = {q.o_c, q.o_e, q.o_n, q.o_nw, q.o_s, q.o_se, q.o_w, q.o_c,
+                          q.o_e, q.o_nw, q.o_n, q.o_se, q.o_s, q.o_w, q.o_c};
+#pragma unroll
+    for (int t = 0; t < 24; ++t) {
+      double P[4][3], uv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const int w = kFemTet[t][a];  // compile-time after unrolling
+        const int o = ocol[w];
+        const double* pp = w <= 3 ? Pl0 : (w <= 10 ? Pl1 : Pl2);
+        const double* up = w <= 3 ? Ul0 : (w <= 10 ? Ul1 : Ul2);
+        P[a][0] = pp[o];
+        P[a][1] = pp[slot_len + o];
+        P[a][2] = pp[2 * slot_len + o];
+        uv[a] = up[o];
+      }
+      double e1[3], e2[3], e3[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        e1[d] = P[1][d] - P[0][d];
+        e2[d] = P[2][d] - P[0][d];
+        e3[d] = P[3][d] - P[0][d];
+      }
+      const double c23[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
+                             e2[0] * e3[1] - e2[1] * e3[0]};
+      const double c31[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2],
+                             e3[0] * e1[1] - e3[1] * e1[0]};
+      const double c12[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                             e1[0] * e2[1] - e1[1] * e2[0]};
+      const double det = e1[0] * c23[0] + e1[1] * c23[1] + e1[2] * c23[2];
+      // |T| grad(l_m).grad(l_a) = |det|/6 (c_m . c_a) / det^2 with c_a = det grad(l_a)
+      const double inv = 1.0 / det;
+      double g[4][3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        g[1][d] = c23[d] * inv;
+        g[2][d] = c31[d] * inv;
+        g[3][d] = c12[d] * inv;
+        g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
+      }
+      const double vol = fabs(det) * (1.0 / 6.0);
+      const int m = t & 3;
+      double ti = 0.0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) ti = fma(g[m][0] * g[a][0] + g[m][1] * g[a][1] + g[m][2] * g[a][2], uv[a], ti);
+      acc = fma(vol, ti, acc);
+      asm volatile("" ::: "memory");  // keep one tet's loads live at a time (register pressure)
+    }
+    optr[sm.po[k]] = (MODE == kModeResid) ? fv - acc : acc;
+  }
+}
+
+}  // namespace hhg

@@ -14,6 +14,7 @@
 #include "pmarch.cuh"
 #include "pair.cuh"
 #include "gsq.cuh"
+#include "femmarch.cuh"
 
 namespace hhg {
 
@@ -512,6 +513,25 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
       return mode == kModeApply ? launch_apply_vol<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
                                 : launch_apply_vol<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
     }
+  }
+  if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !force_v1() && !lv.bands.empty()) {
+    const size_t smem = fem_smem_bytes(lv.slot_len, lv.N);
+    static bool attr = false;
+    if (!attr) {
+      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+      attr = true;
+    }
+    const int nb = (int)lv.bands.size();
+    ProfScope ps(c, 0);
+    if (mode == kModeApply)
+      k_vol_fem<kModeApply><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
+          lv.N, lv.S, lv.d_bands, nb, lv.slot_len, c->d_geo, c->blended, u, f, out);
+    else
+      k_vol_fem<kModeResid><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
+          lv.N, lv.S, lv.d_bands, nb, lv.slot_len, c->d_geo, c->blended, u, f, out);
+    HHG_LAUNCHED(c);
+    return HHG_OK;
   }
   dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
   ProfScope ps(c, mode == kModeGS ? 1 : 0);
