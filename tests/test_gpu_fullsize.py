@@ -7,6 +7,8 @@ one by one from its own definitions:
   oracle's own LSQP fit of the node's macro (PAPER.md:618-636, 647-673);
 * apply at face / edge / vertex nodes: the exact FEM row by node-wise
   assembly over the macros containing the node (PAPER.md:385-394, 632-636);
+* the on-the-fly FEM operator at volume nodes: the oracle's node stencils
+  from the 24 incident fine tets (fem.volume_stencils, PAPER.md:385-394);
 * GS at volume nodes >= 5 lattice steps from their macro's boundary: the
   colour-ordered update (R13/R14) replayed on the node's dependency
   cone -- a colour-c node reads new values of its lower-colour neighbours,
@@ -51,9 +53,12 @@ def case(t, nr, L):
     dy, dr = ctx.zeros(L), ctx.zeros(L)
     ctx.apply(L, du, dy)
     ctx.residual(L, du, df, dr)
+    dfem = ctx.zeros(L)
+    ctx.apply(L, du, dfem, op="fem")
     ctx.gs_sweep(L, du, df, 1)
     torch.cuda.synchronize()
-    out = {"y": ctx.gather_global(L, dy), "r": ctx.gather_global(L, dr), "ug": ctx.gather_global(L, du)}
+    out = {"y": ctx.gather_global(L, dy), "r": ctx.gather_global(L, dr), "ug": ctx.gather_global(L, du),
+           "yfem": ctx.gather_global(L, dfem)}
     ctx.close()
     return mesh, num, u, f, out
 
@@ -165,3 +170,19 @@ def test_fullsize_gs_sweep_sampled(t, nr, L):
         ref, scale = new_value(p)
         gI = int(num.gids(T, np.array([p]))[0])
         assert abs(out["ug"][gI] - ref) <= TOL * scale, (T, p, out["ug"][gI], ref)
+
+
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+def test_fullsize_fem_operator_sampled(t, nr, L):
+    mesh, num, u, f, out = case(t, nr, L)
+    N = 2 ** L
+    rng = np.random.default_rng(777 + L)
+    pts = sample_volume(rng, N, mesh.nt, 48, 1)
+    for T, i, j, k in pts:
+        ijk = np.array([[i, j, k]])
+        sw = fem.volume_stencils(mesh, T, ijk, N, blended=True)[0]
+        gI = int(num.gids(T, ijk)[0])
+        un = u[num.gids(T, ijk + DIRS)]
+        ref = float(np.dot(sw, un))
+        scale = float(np.abs(sw * un).sum())
+        assert abs(out["yfem"][gI] - ref) <= TOL * scale, (T, i, j, k, out["yfem"][gI], ref)

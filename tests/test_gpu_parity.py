@@ -127,7 +127,7 @@ def test_apply_residual_gs_match_oracle(mesh_name, L):
     assert rel(ctx.gather_global(L, ug), u_ref) < TOL
 
 
-@pytest.mark.parametrize("mesh_name,L", [("tet", 4), ("shell60", 3), ("flat_tet", 4)])
+@pytest.mark.parametrize("mesh_name,L", [("tet", 4), ("tet", 6), ("tet", 7), ("shell60", 3), ("flat_tet", 4)])
 def test_fem_and_const_operators(mesh_name, L):
     mesh, num, Lt, A, cf = oracle_case(mesh_name, L)
     ctx = gpu_ctx(mesh_name, L)
