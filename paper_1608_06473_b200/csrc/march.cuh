@@ -29,7 +29,7 @@ namespace hhg {
 
 // Optional cycle accounting of the GS kernels (build with -DHHG_GS_PROF; tools/gsprof.py).
 #ifdef HHG_GS_PROF
-__device__ unsigned long long g_gsprof[8];
+__device__ unsigned long long g_gsprof[12];
 #define GPROF_T0 long long _t0 = clock64();
 #define GPROF_ADD(i) if (threadIdx.x == 0) atomicAdd(&g_gsprof[i], (unsigned long long)(clock64() - _t0));
 #else
@@ -424,6 +424,9 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
                                                  int colour, double* __restrict__ ub, const double* __restrict__ fb,
                                                  double* __restrict__ wb, const Gate& gate = Gate()) {
   constexpr int NQ = RING / 4;
+#ifdef HHG_GS_PROF
+  long long _tp0 = clock64();
+#endif
   if (threadIdx.x == 0) {
     for (int s = 0; s < NQ; ++s) mbar_init(&sm.bars[s], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -468,6 +471,9 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
   const int nsteps = (b.kmax + 4) / 4;
   double f_next = 0.0;
   if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
+#ifdef HHG_GS_PROF
+  if (threadIdx.x == 0) atomicAdd(&g_gsprof[8], (unsigned long long)(clock64() - _tp0));
+#endif
   for (int s = 0; s < nsteps; ++s) {
     {
       GPROF_T0
@@ -527,7 +533,9 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
       next_quad = max(next_quad, to + 1);
     }
   }
+  GPROF_T0
   wait_quads(last_quad);  // every issued quad is consumed before the barriers are re-initialised
+  GPROF_ADD(9)
 }
 
 template <int OP, int RING = kRing>
@@ -622,7 +630,11 @@ __global__ void __launch_bounds__(NT, 512 / NT)
                                      u + T * S + q.c);
         else
           gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
-        __syncthreads();
+        {
+          GPROF_T0
+          __syncthreads();
+          GPROF_ADD(10)
+        }
         GPROF_ADD(1)
       }
       // bar.sync orders every thread's stores before thread 0's gpu-scope fence (cumulative)

@@ -837,8 +837,8 @@ extern "C" hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, 
 
 #ifdef HHG_GS_PROF
 extern "C" int hhg_gs_prof_read(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, hhg::g_gsprof, 8 * sizeof(unsigned long long));
-  unsigned long long z[8] = {0};
+  cudaMemcpyFromSymbol(out, hhg::g_gsprof, 12 * sizeof(unsigned long long));
+  unsigned long long z[12] = {0};
   cudaMemcpyToSymbol(hhg::g_gsprof, z, sizeof(z));
   return 0;
 }

@@ -16,7 +16,7 @@ u, f = ctx.zeros(L), ctx.zeros(L)
 ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(0, g)).cuda(), u)
 ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(1, g)).cuda(), f)
 lib = hhg.lib()
-buf = (ctypes.c_ulonglong * 8)()
+buf = (ctypes.c_ulonglong * 12)()
 ctx.gs_sweep(L, u, f, 1); torch.cuda.synchronize(); lib.hhg_gs_prof_read(buf)
 ctx.gs_sweep(L, u, f, 1); torch.cuda.synchronize(); lib.hhg_gs_prof_read(buf)
 v = list(buf)
@@ -26,6 +26,7 @@ if os.environ["HHG_GS_KERNEL"] == "quad":
         tot, 100 * v[0] / tot, 100 * v[1] / tot, 100 * v[2] / tot, v[4], tot / max(v[4], 1)))
 else:
     print("items: CTA-cycles total %.3e: flag waits %.1f%%, passes %.1f%% (of which refill issue %.1f%%, "
-          "quad waits %.1f%%, node compute %.1f%%, refill barrier %.1f%%), item setup %.1f%%" % (
+          "quad waits %.1f%%, node compute %.1f%%, refill barrier %.1f%%, pass start %.1f%%, final waits %.1f%%, "
+          "end barrier %.1f%%), item setup %.1f%%" % (
               tot, 100 * v[0] / tot, 100 * v[1] / tot, 100 * v[2] / tot, 100 * v[5] / tot, 100 * v[6] / tot,
-              100 * v[7] / tot, 100 * v[4] / tot))
+              100 * v[7] / tot, 100 * v[8] / tot, 100 * v[9] / tot, 100 * v[10] / tot, 100 * v[4] / tot))
