@@ -6,6 +6,7 @@
 // PAPER.md:862-871 (residual), PAPER.md:1306-1315 (eq. iteration-scheme:
 // u_I = (f_I - sum_{w != mc} s_w u_{I_w}) / s_mc).
 #include <cstring>
+#include <map>
 
 #include "fem_device.cuh"
 #include "hhg_internal.h"
@@ -397,14 +398,16 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
   int* flags = narrow ? lv.d_gs_flags_s : lv.d_gs_flags;
   const int slot_len = narrow ? lv.slot_len_s : lv.slot_len;
   const size_t smem = march_smem_bytes(slot_len, lv.N, RING);
-  static int grid = 0;
+  // persistent grid: every CTA resident (the flag waits rely on it), sized for
+  // this level's ring
+  static std::map<size_t, int> grids;
+  int& grid = grids[smem];
   if (grid == 0) {
     HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
     int dev = 0, sms = 0, per_sm = 0;
     HHG_CK(c, cudaGetDevice(&dev));
     HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT, RING>, NT,
-                                                            march_smem_bytes(narrow ? 400 : 520, 256, RING)));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT, RING>, NT, smem));
     grid = sms * std::max(per_sm, 1);
   }
   const int nb = (int)bands.size();

@@ -17,6 +17,9 @@ import torch
 import paper_1608_06473_b200 as hhg
 import synth
 
+if os.environ.get("KB_LIB"):  # variant build of the library (tools/prof/*.so)
+    hhg.LIB_PATH = os.path.abspath(os.environ["KB_LIB"])
+
 
 def main():
     t = int(sys.argv[1]) if len(sys.argv) > 1 else 1
@@ -58,6 +61,11 @@ def main():
         ctx.profile(False)
         parts = " ".join(f"{k}={v[0] / reps:.3f}" for k, v in prof.items() if v[1])
         print(f"{tag} {name}: {ms:.3f} ms/call  {n_owned / ms / 1e6:.1f} GLUP/s  [{parts}]", flush=True)
+    if os.environ.get("KB_CHECK"):  # fingerprint of one GS sweep from the seeded start (variant cross-check)
+        ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(0, g)).cuda(), u)
+        ctx.gs_sweep(L, u, f, 2)
+        ug = np.asarray(ctx.gather_global(L, u), dtype=np.float64)
+        print(f"{tag} check: sum={ug.sum():.17e} sumsq={np.dot(ug, ug):.17e}", flush=True)
     ctx.close()
 
 
