@@ -321,9 +321,20 @@ def main():
            "roofline": roof,
            "clocks": clk.summary(),
            "profile_ms": prof}
-    if rank == 0 and not a.no_extras:
-        out["e2e"] = e2e(ctx, L, u, f, y, a, n_owned_total, 1)
-        out["comparisons"] = comparisons(ctx, L, u, f, y, n_owned) if ws == 1 else None
+    if not a.no_extras:
+        # every rank takes part (apply / GS / V-cycle are collectives over the
+        # ranks' ghost exchange); times are the max over ranks
+        def tmax(x):
+            if not dist:
+                return x
+            tt = torch.tensor([float(x)], device=rdev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            return float(tt.item())
+        ee = e2e(ctx, L, u, f, y, a, n_owned_total, tmax)
+        cmp = comparisons(ctx, L, u, f, y, n_owned_total, tmax)
+        if rank == 0:
+            out["e2e"] = ee
+            out["comparisons"] = cmp
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(L, q)
     if rank == 0:
@@ -333,7 +344,7 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e(ctx, L, u, f, y, a, n_owned, ws):
+def e2e(ctx, L, u, f, y, a, n_owned, tmax):
     """Same metric through the C-ABI with HOST buffers: the library stages
     u (apply), u and f (GS) host->device and y, u device->host every step."""
     import torch
@@ -348,13 +359,13 @@ def e2e(ctx, L, u, f, y, a, n_owned, ws):
     for _ in range(n):
         step()
     torch.cuda.synchronize()
-    t = (time.perf_counter() - t0) / n
+    t = tmax((time.perf_counter() - t0) / n)
     nb = hu.numel() * 8
-    return {"value": 2 * n_owned * ws / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": 3 * nb,
+    return {"value": 2 * n_owned / t / 1e9, "unit": UNIT, "h2d_bytes_per_step": 3 * nb,
             "d2h_bytes_per_step": 2 * nb, "ms_per_step": t * 1e3}
 
 
-def comparisons(ctx, L, u, f, y, n_owned):
+def comparisons(ctx, L, u, f, y, n_owned, tmax):
     """Comparison operators on the same workload (a11/a12): element-wise
     on-the-fly FEM apply and constant-stencil (affine) apply, GLUP/s."""
     import torch
@@ -368,7 +379,7 @@ def comparisons(ctx, L, u, f, y, n_owned):
             ctx.apply(L, u, y, op=op)
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / reps
+        ms = tmax(e0.elapsed_time(e1) / reps)
         res[f"{op}_apply"] = {"ms": ms, "glups": n_owned / (ms * 1e-3) / 1e9}
     # BASELINE config 5 on this GPU's mesh: V(3,3) cycles, levels 2..L, surrogate
     # GS smoother on every level, 50 CG iterations at L = 2 (u, f ~ U[-1,1]).
@@ -384,7 +395,7 @@ def comparisons(ctx, L, u, f, y, n_owned):
     e1.record()
     torch.cuda.synchronize()
     rates = [hist[i + 1] / hist[i] for i in range(ncyc) if hist[i] > 0]
-    res["vcycle_V33"] = {"ms_per_cycle": e0.elapsed_time(e1) / ncyc, "levels": f"2..{L}",
+    res["vcycle_V33"] = {"ms_per_cycle": tmax(e0.elapsed_time(e1) / ncyc), "levels": f"2..{L}",
                          "residual_history": [float(h) for h in hist],
                          "reduction_per_cycle": [float(r) for r in rates]}
     return res

@@ -150,14 +150,18 @@ hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, const double* 
  * operator, prolongation P (index-space linear interpolation, R18).
  * res_hist[n_cycles+1] (host, may be NULL) receives ||f - A u||_2 before the
  * first and after every cycle.  Returns HHG_ERR_DIVERGED if the residual grew
- * three cycles in a row (history still written). */
+ * three cycles in a row (history still written).  Multi-rank: a collective
+ * like hhg_apply; the restriction sums the partials of copies on other ranks
+ * into the owner (reverse exchange) before the owners' totals are re-synced. */
 hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
                       hhg_op op, double* u, const double* f, int n_cycles, double* res_hist);
 
 /* Canonical global vector (length n_global_nodes, DESIGN.md numbering:
  * vertices, edges, faces, volumes) <-> local layout.  gather writes every
  * node (0 at Dirichlet); scatter writes every copy and zeroes Dirichlet slots.
- * Single-rank contexts only in this version (HHG_ERR_INVALID otherwise). */
+ * Multi-rank: gather writes the entries this rank owns and 0 elsewhere (the sum
+ * over ranks is the global vector); scatter takes the full global vector on
+ * every rank. */
 hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local, double* global_vec);
 hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* global_vec, double* local);
 

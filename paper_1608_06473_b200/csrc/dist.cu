@@ -187,7 +187,26 @@ hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_
   }
   lv.n_send = nsend;
   lv.n_recv = (int64_t)lv.h_recv_slot.size();
+  // reverse grouping: one owner slot may be requested by several peers / copies
+  std::vector<uint32_t> rptr, rslot, ridx(nsend);
+  for (int64_t x = 0; x < nsend; ++x) ridx[x] = (uint32_t)x;
+  std::stable_sort(ridx.begin(), ridx.end(),
+                   [&](uint32_t a, uint32_t b) { return lv.h_send_slot[a] < lv.h_send_slot[b]; });
+  for (int64_t x = 0; x < nsend; ++x) {
+    if (x == 0 || lv.h_send_slot[ridx[x]] != lv.h_send_slot[ridx[x - 1]]) {
+      rptr.push_back((uint32_t)x);
+      rslot.push_back(lv.h_send_slot[ridx[x]]);
+    }
+  }
+  rptr.push_back((uint32_t)nsend);
+  lv.n_rsum = (int64_t)rslot.size();
   if (c->host_only) return HHG_OK;
+  HHG_CK(c, cudaMalloc(&lv.d_rsum_ptr, rptr.size() * 4));
+  HHG_CK(c, cudaMalloc(&lv.d_rsum_slot, std::max<int64_t>(lv.n_rsum, 1) * 4));
+  HHG_CK(c, cudaMalloc(&lv.d_rsum_idx, std::max<int64_t>(nsend, 1) * 4));
+  HHG_CK(c, cudaMemcpy(lv.d_rsum_ptr, rptr.data(), rptr.size() * 4, cudaMemcpyHostToDevice));
+  if (lv.n_rsum) HHG_CK(c, cudaMemcpy(lv.d_rsum_slot, rslot.data(), lv.n_rsum * 4, cudaMemcpyHostToDevice));
+  if (nsend) HHG_CK(c, cudaMemcpy(lv.d_rsum_idx, ridx.data(), nsend * 4, cudaMemcpyHostToDevice));
   HHG_CK(c, cudaMalloc(&lv.d_send_slot, std::max<int64_t>(lv.n_send, 1) * 4));
   HHG_CK(c, cudaMalloc(&lv.d_recv_slot, std::max<int64_t>(lv.n_recv, 1) * 4));
   HHG_CK(c, cudaMalloc(&lv.d_sendbuf, std::max<int64_t>(lv.n_send, 1) * 8));
@@ -227,6 +246,43 @@ hhg_status dist_sync(Ctx* c, Level& lv, double* v) {
   if (st != HHG_OK) return st;
   if (lv.n_recv) {
     k_unpack<<<(unsigned)((lv.n_recv + 255) / 256), 256, 0, c->stream>>>(lv.n_recv, lv.d_recv_slot, lv.d_recvbuf, v);
+    HHG_LAUNCHED(c);
+  }
+  return HHG_OK;
+}
+
+// owner slot += the copies' partial values (fixed order: deterministic)
+__global__ void k_unpack_sum(int64_t n, const uint32_t* __restrict__ ptr, const uint32_t* __restrict__ slot,
+                             const uint32_t* __restrict__ idx, const double* __restrict__ buf,
+                             double* __restrict__ v) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double s = 0.0;
+  for (uint32_t e = ptr[t]; e < ptr[t + 1]; ++e) s += buf[idx[e]];
+  v[slot[t]] += s;
+}
+
+// Reverse of dist_sync: every mirrored slot sends its value to the owner,
+// which adds them into its authoritative slot (restriction partial sums,
+// PAPER.md:852-860 R = P^T across a rank boundary).  The mirrored slots keep
+// their values; callers re-sync after summing the owner's local copies.
+hhg_status dist_sum_to_owner(Ctx* c, Level& lv, double* v) {
+  if (c->nranks == 1) return HHG_OK;
+  ProfScope ps(c, 3);
+  if (lv.n_recv) {
+    k_pack<<<(unsigned)((lv.n_recv + 255) / 256), 256, 0, c->stream>>>(lv.n_recv, lv.d_recv_slot, v, lv.d_recvbuf);
+    HHG_LAUNCHED(c);
+  }
+  std::vector<int64_t> sb(c->nranks), rb(c->nranks);
+  for (int p = 0; p < c->nranks; ++p) {
+    sb[p] = lv.recv_cnt[p] * 8;
+    rb[p] = lv.send_cnt[p] * 8;
+  }
+  hhg_status st = dist_exchange_bytes(c, sb, lv.d_recvbuf, rb, lv.d_sendbuf, true);
+  if (st != HHG_OK) return st;
+  if (lv.n_rsum) {
+    k_unpack_sum<<<(unsigned)((lv.n_rsum + 255) / 256), 256, 0, c->stream>>>(lv.n_rsum, lv.d_rsum_ptr, lv.d_rsum_slot,
+                                                                             lv.d_rsum_idx, lv.d_sendbuf, v);
     HHG_LAUNCHED(c);
   }
   return HHG_OK;

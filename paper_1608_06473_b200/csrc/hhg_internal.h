@@ -186,6 +186,12 @@ struct Level {
   double* d_sendbuf = nullptr;
   double* d_recvbuf = nullptr;
   int64_t n_send = 0, n_recv = 0;
+  // reverse direction (copies -> owner, summed): the send entries grouped by
+  // owner slot, entries of a slot in (peer rank, request) order
+  int64_t n_rsum = 0;
+  uint32_t* d_rsum_ptr = nullptr;   // [n_rsum + 1]
+  uint32_t* d_rsum_slot = nullptr;  // [n_rsum]
+  uint32_t* d_rsum_idx = nullptr;   // [n_send]
   // persistent GS work queue (k_gs_items)
   int* d_gs_flags = nullptr;   // [nt_local][n_bands][4] sweep epoch of completed colour passes
   int* d_gs_counter = nullptr; // [1]
@@ -301,6 +307,7 @@ hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_
                            const std::vector<int64_t>& recv_gid, const std::vector<int32_t>& recv_rank,
                            const std::vector<std::pair<int64_t, uint32_t>>& serve);
 hhg_status dist_sync(Ctx* c, Level& lv, double* v);
+hhg_status dist_sum_to_owner(Ctx* c, Level& lv, double* v);
 hhg_status dist_allreduce_sum(Ctx* c, double* d_scalar);
 
 // Structured face rows (faces.cu)

@@ -10,6 +10,9 @@
 // nodes it OWNS (lowest macro id containing the node's primitive) into partial
 // sums at its copies of the coarse nodes, then the copies of shared coarse
 // nodes are summed (hhg::lp_sum_copies), so every fine node counts once.
+// Multi-rank: each rank restricts its own macros; copies on other ranks reach
+// the owner through dist_sum_to_owner (the reverse of the ghost sync), and
+// prolongation re-syncs the ghost slots it cannot compute.
 #include <cmath>
 
 #include "fem_device.cuh"
@@ -158,11 +161,19 @@ static hhg_status restrict_to(Ctx* c, int Lf, const double* rf, double* fc) {
   Level& F = c->levels[Lf];
   Level& C = c->levels[Lf - 1];
   dim3 grid(nblk(C.P, 128), (unsigned)c->nt_local);
+  hhg_status st;
+  if (c->nt_blocks > c->nt_local)  // ghost blocks hold no partial sums
+    HHG_CK(c, cudaMemsetAsync(fc + c->nt_local * C.S, 0, (c->nt_blocks - c->nt_local) * C.S * sizeof(double),
+                              c->stream));
   k_restrict_partial<<<grid, 128, 0, c->stream>>>(F.N, F.S, C.S, C.P, c->d_own, rf, fc);
   HHG_LAUNCHED(c);
-  hhg_status st = lp_sum_copies(c, C, fc);
-  if (st != HHG_OK) return st;
-  return zero_dir_slots(c, C, fc);
+  // multi-rank: the partials at the copies of shared coarse nodes on other
+  // ranks are added into the owner's slot first, then every rank sums its own
+  // rows' local copies, then the owners' totals go back to every copy
+  if ((st = dist_sum_to_owner(c, C, fc)) != HHG_OK) return st;
+  if ((st = lp_sum_copies(c, C, fc)) != HHG_OK) return st;
+  if ((st = zero_dir_slots(c, C, fc)) != HHG_OK) return st;
+  return dist_sync(c, C, fc);
 }
 
 static hhg_status prolong_add(Ctx* c, int Lf, const double* uc, double* uf) {
@@ -171,7 +182,7 @@ static hhg_status prolong_add(Ctx* c, int Lf, const double* uc, double* uf) {
   dim3 grid(nblk(F.P, 128), (unsigned)c->nt_local);
   k_prolong_add<<<grid, 128, 0, c->stream>>>(F.N, F.S, C.S, F.P, uc, uf);
   HHG_LAUNCHED(c);
-  return HHG_OK;
+  return dist_sync(c, F, uf);  // ghost-block slots of the other ranks' macros
 }
 
 static hhg_status vcycle_rec(Ctx* c, int L, int Lc, int nu1, int nu2, int cg_iters, int op, double* u,
@@ -209,8 +220,8 @@ extern "C" hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coa
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: bad arguments");
   if (op != HHG_OP_SURROGATE && op != HHG_OP_CONST_AFFINE)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: smoother op must be SURROGATE or CONST_AFFINE");
-  if (c->nranks > 1 || c->host_only)
-    return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: single-rank contexts only in this version");
+  if (c->host_only)
+    return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: needs device vectors (host_only context)");
   for (int l = L_coarse; l <= L; ++l)
     if (!c->levels[l].fitted) return set_err(c, HHG_ERR_STATE, "hhg_vcycle: call hhg_fit_surrogates first");
   hhg_status st = ensure_mg(c);

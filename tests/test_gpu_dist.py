@@ -98,3 +98,72 @@ def test_two_ranks_match_oracle(mesh_args, L):
         assert abs(res[r]["norm"] - np.linalg.norm(r_ref)) < 1e-12 * np.linalg.norm(r_ref)
     u2 = solvers.GS(Lt, num).sweep(u.copy(), f, 2)
     assert rel(res[0]["u"], u2) < 1e-12
+
+
+def _vworker(rank, world, port, mesh_args, L, cycles, out_q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1608_06473_b200 as hhg
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        mesh = synth.shell_mesh(0.55, 1.0, *mesh_args)
+        hhg.set_torch_transport(host_only=False)
+        owner = (np.arange(mesh.nt) * world) // mesh.nt
+        ctx = hhg.Ctx.from_mesh(mesh, L, rank=rank, nranks=world, owner=owner)
+        ctx.fit(2)
+        n_local, n_owned, n_global = ctx.layout(L)
+        g = np.arange(n_global)
+        num = G.Numbering(mesh, 2 ** L)
+        u = synth.uniform_pm1(7, g) * num.unknown_mask
+        f = synth.uniform_pm1(8, g) * num.unknown_mask
+        du, df = ctx.zeros(L), ctx.zeros(L)
+        ctx.scatter_global(L, torch.from_numpy(u).cuda(), du)
+        ctx.scatter_global(L, torch.from_numpy(f).cuda(), df)
+        hist = ctx.vcycle(L, du, df, n_cycles=cycles)
+        torch.cuda.synchronize()
+        part = torch.from_numpy(ctx.gather_global(L, du))
+        dist.all_reduce(part)
+        out_q.put((rank, {"hist": hist, "u": part.numpy()}))
+        ctx.close()
+    except Exception:  # pragma: no cover
+        import traceback
+        out_q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mesh_args,L,cycles", [((0, 2), 4, 3)])
+def test_two_rank_vcycle_matches_oracle(mesh_args, L, cycles):
+    """V(3,3) with the macros split over 2 ranks (restriction partials of
+    shared coarse nodes summed across ranks, prolongation re-synced): residual
+    history and iterate agree with the single-process oracle to 1e-10."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    world = 2
+    procs = [ctx.Process(target=_vworker, args=(r, world, port, mesh_args, L, cycles, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+    mesh = synth.shell_mesh(0.55, 1.0, *mesh_args)
+    H = solvers.Hierarchy(mesh, L, 2, 2)
+    num = H.num[L]
+    g = np.arange(num.n_total)
+    u0 = synth.uniform_pm1(7, g) * num.unknown_mask
+    f = synth.uniform_pm1(8, g) * num.unknown_mask
+    u_ref, hist_ref = H.solve(u0.copy(), f, cycles)
+    for r in range(world):
+        assert np.all(np.abs(res[r]["hist"] - hist_ref) <= 1e-10 * hist_ref), (r, res[r]["hist"], hist_ref)
+    rel = np.linalg.norm(res[0]["u"] - u_ref) / np.linalg.norm(u_ref)
+    assert rel < 1e-10
