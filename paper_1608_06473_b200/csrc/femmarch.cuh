@@ -17,6 +17,7 @@
 namespace hhg {
 
 constexpr int kFRing = 8;  // u plane slots
+constexpr int kFPosPerThread = 3;  // ring columns per thread whose positions it computes
 
 // The 24 fine tets incident to an interior lattice node, as the directions
 // (HHG_DIRS_INIT order; 7 = the node) of their 4 vertices -- fem_partial's
@@ -68,8 +69,9 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   const Column q = make_column(b, N);
   const int clo = b.c_lo;
   // lattice columns of the ring range this thread computes positions for
-  int pc_i[2], pc_j[2];
-  for (int r = 0; r < 2; ++r) {
+  // (ring range <= 3 x 256 columns: N = 256 single-diagonal bands span 3 diagonals)
+  int pc_i[kFPosPerThread], pc_j[kFPosPerThread];
+  for (int r = 0; r < kFPosPerThread; ++r) {
     const int c = clo + (int)threadIdx.x + r * kMarchThreads;
     int d = (int)((sqrt(8.0 * (double)c + 1.0) - 1.0) * 0.5);
     while ((d + 1) * (d + 2) / 2 <= c) ++d;
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   }
   auto positions = [&](int k) {  // plane k -> pos slot k & 3
     double* P = sm.pos + (size_t)(k & 3) * 3 * slot_len;
-    for (int r = 0; r < 2; ++r) {
+    for (int r = 0; r < kFPosPerThread; ++r) {
       const int o = (int)threadIdx.x + r * kMarchThreads;
       if (o >= b.ncols + 1) continue;
       const int i = pc_i[r], j = pc_j[r];

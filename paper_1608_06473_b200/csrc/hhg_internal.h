@@ -108,6 +108,8 @@ struct Band {
   int ncolumns;     // interior columns (threads used)
 };
 constexpr int kMarchThreads = 256;
+// opt-in dynamic shared memory limit of the march kernels (227 KB per block on sm_100, minus static)
+constexpr int kMaxDynSmem = 227 * 1024 - 1024;
 constexpr int kNarrowThreads = 128;
 constexpr int kRing = 16;  // plane slots (power of 2); >= 11 planes in flight ahead of use
 

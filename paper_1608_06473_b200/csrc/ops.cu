@@ -253,7 +253,7 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
   static bool attr = false;
   if (!attr) {
-    HHG_CK(c, cudaFuncSetAttribute(k_vol_march<OP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    HHG_CK(c, cudaFuncSetAttribute(k_vol_march<OP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     attr = true;
   }
   const int nb = (int)lv.bands.size();
@@ -379,7 +379,7 @@ static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, cons
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
   static bool attr = false;
   if (!attr) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_march<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_march<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     attr = true;
   }
   const int nb = (int)lv.bands.size();
@@ -403,7 +403,7 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
   static std::map<size_t, int> grids;
   int& grid = grids[smem];
   if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     int dev = 0, sms = 0, per_sm = 0;
     HHG_CK(c, cudaGetDevice(&dev));
     HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -411,6 +411,10 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
     grid = sms * std::max(per_sm, 1);
   }
   const int nb = (int)bands.size();
+  // deadlock freedom needs every band of the partially handed-out macro
+  // resident at once (an item waits on its neighbour bands): otherwise use the
+  // colour-pass kernels (no cross-CTA waits)
+  if (grid <= nb) return HHG_ERR_STATE;
   // macro group: u and f of G macros (~90 MB) stay L2-resident across the 4
   // colours, and a colour stage (G x bands items) is several CTA waves long so
   // that stage c+1 rarely waits for stage c.
@@ -438,7 +442,7 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
     static bool attr = false;
     if (!attr) {
       HHG_CK(c, cudaFuncSetAttribute(k_gs_items_p<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     110 * 1024));
+                                     kMaxDynSmem));
       attr = true;
     }
     k_gs_items_p<OP, NT, RING><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
@@ -466,7 +470,9 @@ static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f)
     ring = (e && atoi(e) == 16) ? 16 : 24;
   }
   if (nt == 128 && !lv.bands_s.empty()) return launch_gs_items_nt<OP, kNarrowThreads, 24>(c, lv, u, f);
-  if (ring == 16) return launch_gs_items_nt<OP, kMarchThreads, 16>(c, lv, u, f);
+  // 24-plane ring only while two CTAs fit an SM (N = 256: 768-double slots -> 16)
+  if (ring == 16 || march_smem_bytes(lv.slot_len, lv.N, 24) > 113 * 1024)
+    return launch_gs_items_nt<OP, kMarchThreads, 16>(c, lv, u, f);
   return launch_gs_items_nt<OP, kMarchThreads, 24>(c, lv, u, f);
 }
 
@@ -476,7 +482,7 @@ static hhg_status launch_gs_quad(Ctx* c, Level& lv, double* u, const double* f) 
   const size_t smem = gsq_smem_bytes(lv.slot_len, lv.N);
   static int grid = 0;
   if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_quad<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_quad<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     int dev = 0, sms = 0, per_sm = 0;
     HHG_CK(c, cudaGetDevice(&dev));
     HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -484,7 +490,7 @@ static hhg_status launch_gs_quad(Ctx* c, Level& lv, double* u, const double* f) 
                                                             gsq_smem_bytes(520, 256)));
     grid = sms * std::max(per_sm, 1);
   }
-  if (smem > 110 * 1024) return set_err(c, HHG_ERR_INVALID, "gs: band too wide for shared memory");
+  if (smem > (size_t)kMaxDynSmem) return set_err(c, HHG_ERR_INVALID, "gs: band too wide for shared memory");
   const int nb = (int)lv.bands.size();
   if (lv.gs_epoch >= 200000) {  // progress words encode epoch * 8192: restart the epochs
     HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
@@ -519,10 +525,12 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
   }
   if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !force_v1() && !lv.bands.empty()) {
     const size_t smem = fem_smem_bytes(lv.slot_len, lv.N);
+    if (lv.slot_len > kFPosPerThread * kMarchThreads)
+      return set_err(c, HHG_ERR_INVALID, "fem: band ring wider than the position pass");
     static bool attr = false;
     if (!attr) {
-      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
-      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, 110 * 1024));
+      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
       attr = true;
     }
     const int nb = (int)lv.bands.size();
@@ -640,11 +648,11 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
     hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_quad<HHG_OP_SURROGATE>(c, lv, u, f)
                                            : launch_gs_quad<HHG_OP_CONST_AFFINE>(c, lv, u, f);
     if (st != HHG_OK) return st;
-  } else if (march_ok && mode == 2) {
-    hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
-                                           : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
-    if (st != HHG_OK) return st;
+  } else if (march_ok && mode == 2 &&
+             (op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
+                                     : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f)) == HHG_OK) {
   } else {
+    if (c->poisoned) return HHG_ERR_CUDA;
     for (int col = 0; col < 4; ++col) {
       hhg_status st = volume_pass(c, lv, op, kModeGS, col, u, f, u);
       if (st != HHG_OK) return st;

@@ -34,12 +34,18 @@ DIRS = np.array(G.DIRS)
 MC = 7
 
 
+def _mesh(t, nr):
+    # t = None: the single curved tet (BASELINE configs 1/2) at the largest
+    # level the ABI accepts (L = 8, N = 256: the widest bands and rings)
+    return synth.single_tet() if t is None else synth.shell_mesh(0.55, 1.0, t, nr)
+
+
 @functools.lru_cache(maxsize=None)
 def case(t, nr, L):
     import torch
 
     import paper_1608_06473_b200 as hhg
-    mesh = synth.shell_mesh(0.55, 1.0, t, nr)
+    mesh = _mesh(t, nr)
     num = G.Numbering(mesh, 2 ** L)
     ctx = hhg.Ctx.from_mesh(mesh, L)
     ctx.fit(2, "lsqp", 2)
@@ -65,7 +71,7 @@ def case(t, nr, L):
 
 @functools.lru_cache(maxsize=None)
 def coeffs(t, nr, L, T):
-    mesh = synth.shell_mesh(0.55, 1.0, t, nr)
+    mesh = _mesh(t, nr)
     return S.fit_macro(mesh, T, L, 2, "lsqp", 2, blended=True)
 
 
@@ -79,14 +85,14 @@ def sample_volume(rng, N, nt, n, min_dist):
     return out
 
 
-@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7), (None, None, 8)])
 def test_fullsize_apply_residual_sampled(t, nr, L):
     mesh, num, u, f, out = case(t, nr, L)
     N = 2 ** L
     rng = np.random.default_rng(1234 + L)
     pts = sample_volume(rng, N, mesh.nt, 96, 1)
     # include nodes next to every macro face and the farthest corners
-    pts += [(0, 1, 1, 1), (mesh.nt - 1, N - 3, 1, 1), (mesh.nt // 2, 1, N - 3, 1), (7, 1, 1, N - 3)]
+    pts += [(0, 1, 1, 1), (mesh.nt - 1, N - 3, 1, 1), (mesh.nt // 2, 1, N - 3, 1), (min(7, mesh.nt - 1), 1, 1, N - 3)]
     for T, i, j, k in pts:
         ijk = np.array([[i, j, k]])
         sw = S.eval_weights(coeffs(t, nr, L, T), ijk, N, 2)[0]
@@ -103,18 +109,21 @@ def _containing(mesh, verts):
     return [T for T in range(mesh.nt) if all(v in set(int(x) for x in mesh.tets[T]) for v in verts)]
 
 
-@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7), (None, None, 8)])
 def test_fullsize_lower_primitive_rows_sampled(t, nr, L):
     mesh, num, u, f, out = case(t, nr, L)
     N = 2 ** L
     rng = np.random.default_rng(99 + L)
     gids = []
     unk_f = np.nonzero(num.unknown_mask[num.base_f:num.base_v])[0] + num.base_f
-    gids += [int(x) for x in rng.choice(unk_f, 12, replace=False)]
     unk_e = np.nonzero(num.unknown_mask[num.base_e:num.base_f])[0] + num.base_e
-    gids += [int(x) for x in rng.choice(unk_e, 4, replace=False)]
     unk_v = np.nonzero(num.unknown_mask[:num.base_e])[0]
-    gids += [int(x) for x in rng.choice(unk_v, 2, replace=False)]
+    for pool, n in ((unk_f, 12), (unk_e, 4), (unk_v, 2)):
+        if len(pool):
+            gids += [int(x) for x in rng.choice(pool, n, replace=False)]
+    if t is None:  # single tet: every face Dirichlet -> lower-primitive outputs are 0
+        lp = slice(0, num.base_v)
+        assert not np.any(out["y"][lp]) and not np.any(out["r"][lp]) and not np.any(out["ug"][lp])
     for g in gids:
         if g >= num.base_f:
             verts = num.faces[(g - num.base_f) // num.nfi]
@@ -132,7 +141,7 @@ def test_fullsize_lower_primitive_rows_sampled(t, nr, L):
         assert abs(out["r"][g] - (f[g] - ref)) <= TOL * (scale + abs(f[g])), g
 
 
-@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7), (None, None, 8)])
 def test_fullsize_gs_sweep_sampled(t, nr, L):
     mesh, num, u, f, out = case(t, nr, L)
     N = 2 ** L
@@ -172,7 +181,7 @@ def test_fullsize_gs_sweep_sampled(t, nr, L):
         assert abs(out["ug"][gI] - ref) <= TOL * scale, (T, p, out["ug"][gI], ref)
 
 
-@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7)])
+@pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7), (None, None, 8)])
 def test_fullsize_fem_operator_sampled(t, nr, L):
     mesh, num, u, f, out = case(t, nr, L)
     N = 2 ** L
