@@ -7,9 +7,12 @@
 // recomputed per tet is shared here: every blended node position is computed
 // once per call (plane by plane into a 4-plane shared-memory ring, by the
 // threads of the band) and the 24 incident tets of an interior node come from
-// a fixed direction table, so a node costs 24 x (gradients, 1 division, 4
-// dot products) ~ 1.6 kflop.  Same arithmetic as the oracle's definition
-// (blended vertices, K_T = |T| grad(l_a).grad(l_b)), summation order differs.
+// a fixed direction table.  Per tet the row entry needs only
+// sum_a K_T[m][a] u_a = |T| grad(l_m).grad(u_h): 3 cross products, the
+// determinant, grad(u_h) from 3 differences, one dot product and one division
+// (~55 fp64 instructions, ~1.3 k per node).  Same quantity as the oracle's
+// definition (blended vertices, K_T = |T| grad(l_a).grad(l_b)); the order of
+// the arithmetic differs.
 #pragma once
 #include "fem_device.cuh"
 #include "march.cuh"
@@ -151,22 +154,20 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
       const double c12[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
                              e1[0] * e2[1] - e1[1] * e2[0]};
       const double det = e1[0] * c23[0] + e1[1] * c23[1] + e1[2] * c23[2];
-      // |T| grad(l_m).grad(l_a) = |det|/6 (c_m . c_a) / det^2 with c_a = det grad(l_a)
-      const double inv = 1.0 / det;
-      double g[4][3];
+      // sum_a |T| grad(l_m).grad(l_a) u_a = |T| grad(l_m).grad(u_h), and with
+      // c_a = det grad(l_a) (a = 1..3, c_0 = -(c_1 + c_2 + c_3)) and
+      // det grad(u_h) = sum_{a>=1} c_a (u_a - u_0) =: G this is (c_m . G) / (6 |det|)
+      const double du1 = uv[1] - uv[0], du2 = uv[2] - uv[0], du3 = uv[3] - uv[0];
+      double G[3];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        g[1][d] = c23[d] * inv;
-        g[2][d] = c31[d] * inv;
-        g[3][d] = c12[d] * inv;
-        g[0][d] = -(g[1][d] + g[2][d] + g[3][d]);
-      }
-      const double vol = fabs(det) * (1.0 / 6.0);
+      for (int d = 0; d < 3; ++d) G[d] = fma(c23[d], du1, fma(c31[d], du2, c12[d] * du3));
       const int m = t & 3;
-      double ti = 0.0;
+      double cm[3];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) ti = fma(g[m][0] * g[a][0] + g[m][1] * g[a][1] + g[m][2] * g[a][2], uv[a], ti);
-      acc = fma(vol, ti, acc);
+      for (int d = 0; d < 3; ++d)
+        cm[d] = m == 1 ? c23[d] : m == 2 ? c31[d] : m == 3 ? c12[d] : -(c23[d] + c31[d] + c12[d]);
+      const double dot = fma(cm[0], G[0], fma(cm[1], G[1], cm[2] * G[2]));
+      acc = fma(dot, 1.0 / (6.0 * fabs(det)), acc);
       asm volatile("" ::: "memory");  // keep one tet's loads live at a time (register pressure)
     }
     optr[sm.po[k]] = (MODE == kModeResid) ? fv - acc : acc;

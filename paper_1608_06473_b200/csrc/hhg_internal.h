@@ -157,6 +157,8 @@ struct Level {
   double* d_cons = nullptr;        // [nt_local][15] affine constant stencil
   double* d_coef10 = nullptr;      // [nt_local][15][10] q<=2 coefficients zero-padded to q=2
   double* d_cC = nullptr;          // [nt_local][15] k^2 coefficients (coef10[..][9]), march kernels
+  double* d_ew_lo = nullptr;       // [n_local] element-wise FEM: sums for the next band's first diagonal
+  double* d_ew_hi = nullptr;       // [n_local] ... for the previous band's last diagonal
   bool fitted = false;
   // column-march bands (<= kMarchThreads columns) and narrow bands (<= kNarrowThreads)
   std::vector<Band> bands;
