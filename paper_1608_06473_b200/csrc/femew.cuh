@@ -128,38 +128,26 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
     }
   };
 
-  // ---- anchor columns: every column (faces included) of diagonals [a_lo, a_hi].
-  // The last band also owns diagonal N-1 (cubes of slab 0 only): of those, only
-  // the tets YZX, ZXY, ZYX reach an interior node (corners 4, 6 on diagonal
-  // N-2, plane 1); the others touch only nodes of the face i+j+k = N.
-  const int a_hi = bi == n_bands - 1 ? N - 1 : b.d1 - 1;
+  // ---- anchor column of this thread: every column (faces included) of the
+  // band's diagonals [a_lo, d1) -- at most kMarchThreads (fem bands, setup.cu)
   const int an_lo = (int)col_idx(a_lo, 0) - clo;
-  const int an_n = (int)col_idx(0, a_hi) + 1 - clo - an_lo;
-  struct Anchor {
-    int lim;     // last slab k0 of the cube column (N-1-d), -1: none
-    uint8_t tm;  // valid Kuhn tets (bit t)
-    int o[8];    // ring offsets of the 8 corner columns
+  const int an_n = (int)col_idx(0, b.d1 - 1) + 1 - clo - an_lo;
+  int an_lim = -1, an_o[8];
+  uint8_t an_tm = 0;
+  auto anchor_setup = [&](int col, int& lim, uint8_t& tm, int (&o)[8]) {
+    int i0, j0;
+    col_ij(col, i0, j0);
+    lim = N - 1 - (i0 + j0);
+    tm = 0x3f;
+    if (i0 == 0) tm &= (1 << 0) | (1 << 1) | (1 << 4);  // X before Y
+    if (j0 == 0) tm &= (1 << 0) | (1 << 2) | (1 << 3);  // Y before Z
+    if (i0 + j0 == N - 1) tm &= (1 << 3) | (1 << 4) | (1 << 5);  // corners 1, 3 lie on diagonal N
+    const int di[8] = {0, 1, -1, 0, 0, 1, -1, 0};
+    const int dj[8] = {0, 0, 1, 1, -1, -1, 0, 0};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) o[c] = ring_off(i0 + di[c], j0 + dj[c], clo, slot_len);
   };
-  Anchor an[2];
-#pragma unroll
-  for (int r = 0; r < 2; ++r) {
-    const int x = (int)threadIdx.x + r * kMarchThreads;
-    an[r].lim = -1;
-    if (x < an_n) {
-      int i0, j0;
-      col_ij(clo + an_lo + x, i0, j0);
-      an[r].lim = N - 1 - (i0 + j0);
-      uint8_t tm = 0x3f;
-      if (i0 == 0) tm &= (1 << 0) | (1 << 1) | (1 << 4);  // X before Y
-      if (j0 == 0) tm &= (1 << 0) | (1 << 2) | (1 << 3);  // Y before Z
-      if (i0 + j0 == N - 1) tm &= (1 << 3) | (1 << 4) | (1 << 5);  // corners 1, 3 lie on diagonal N
-      an[r].tm = tm;
-      const int di[8] = {0, 1, -1, 0, 0, 1, -1, 0};
-      const int dj[8] = {0, 0, 1, 1, -1, -1, 0, 0};
-#pragma unroll
-      for (int c = 0; c < 8; ++c) an[r].o[c] = ring_off(i0 + di[c], j0 + dj[c], clo, slot_len);
-    }
-  }
+  if ((int)threadIdx.x < an_n) anchor_setup(clo + an_lo + (int)threadIdx.x, an_lim, an_tm, an_o);
   // ---- output nodes: the band's interior columns, and the halo diagonals' nodes
   const Column q = make_column(b.d0 == 2 ? bands[bi] : b, N);  // offsets relative to the band's own c_lo
   const int qshift = bands[bi].c_lo - clo;                       // -> relative to this kernel's clo
@@ -169,68 +157,84 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   // d0, top corners) and of diagonal d1 (anchors on d1-1, bottom corners)
   const int nh_lo = (b.d0 - 1 >= 2 && bi > 0) ? b.d0 - 2 : 0;        // (i,j) i,j >= 1 on diagonal d0-1
   const int nh_hi = (b.d1 <= N - 2 && bi < n_bands - 1) ? b.d1 - 1 : 0;  // on diagonal d1
+  // corner sums sum_b K_ab u_b of the valid Kuhn tets of one cube, corners from
+  // shared memory (P0/U0: plane k0, P1/U1: plane k0+1)
+  auto cube = [&](const int (&o)[8], uint8_t tm, const double* P0, const double* P1, const double* U0,
+                  const double* U1, double (&yc)[8]) {
+    double P[8][3], U[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double* pp = c < 4 ? P0 : P1;
+      P[c][0] = pp[o[c]];
+      P[c][1] = pp[slot_len + o[c]];
+      P[c][2] = pp[2 * slot_len + o[c]];
+      U[c] = (c < 4 ? U0 : U1)[o[c]];
+    }
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      if (!((tm >> t) & 1)) continue;
+      const int v0 = kKuhn[t][0], v1 = kKuhn[t][1], v2 = kKuhn[t][2], v3 = kKuhn[t][3];
+      double e1[3], e2[3], e3[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        e1[d] = P[v1][d] - P[v0][d];
+        e2[d] = P[v2][d] - P[v0][d];
+        e3[d] = P[v3][d] - P[v0][d];
+      }
+      const double c1[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
+                            e2[0] * e3[1] - e2[1] * e3[0]};
+      const double c2[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2],
+                            e3[0] * e1[1] - e3[1] * e1[0]};
+      const double c3[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
+                            e1[0] * e2[1] - e1[1] * e2[0]};
+      const double det = e1[0] * c1[0] + e1[1] * c1[1] + e1[2] * c1[2];
+      const double du1 = U[v1] - U[v0], du2 = U[v2] - U[v0], du3 = U[v3] - U[v0];
+      double G[3];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) G[d] = fma(c1[d], du1, fma(c2[d], du2, c3[d] * du3));
+      const double s = 1.0 / (6.0 * fabs(det));
+      const double y1 = fma(c1[0], G[0], fma(c1[1], G[1], c1[2] * G[2])) * s;
+      const double y2 = fma(c2[0], G[0], fma(c2[1], G[1], c2[2] * G[2])) * s;
+      const double y3 = fma(c3[0], G[0], fma(c3[1], G[1], c3[2] * G[2])) * s;
+      yc[v1] += y1;
+      yc[v2] += y2;
+      yc[v3] += y3;
+      yc[v0] -= (y1 + y2) + y3;  // rows of K_T sum to zero
+    }
+  };
   auto slab_sums = [&](int k0) {
     double* const topb = sm.top + (size_t)(k0 & 1) * 4 * slot_len;
     const double* P0 = sm.pos + (size_t)(k0 & 1) * 3 * slot_len;
     const double* P1 = sm.pos + (size_t)((k0 + 1) & 1) * 3 * slot_len;
     const double* U0 = sm.ring + (k0 % kEwRing) * slot_len + ((sm.po[k0] + clo) & 1);
     const double* U1 = sm.ring + ((k0 + 1) % kEwRing) * slot_len + ((sm.po[k0 + 1] + clo) & 1);
-#pragma unroll 1
-    for (int r = 0; r < 2; ++r) {
-      const int x = (int)threadIdx.x + r * kMarchThreads;
-      if (x >= an_n) break;
-      const int oa = an_lo + x;
+    if ((int)threadIdx.x < an_n) {
+      const int oa = an_lo + (int)threadIdx.x;
       double yc[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) yc[c] = 0.0;
-      if (k0 <= an[r].lim) {
-        double P[8][3], U[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const double* pp = c < 4 ? P0 : P1;
-          const int o = an[r].o[c];
-          P[c][0] = pp[o];
-          P[c][1] = pp[slot_len + o];
-          P[c][2] = pp[2 * slot_len + o];
-          U[c] = (c < 4 ? U0 : U1)[o];
-        }
-        const uint8_t tm = an[r].tm;
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          if (!((tm >> t) & 1)) continue;
-          const int v0 = kKuhn[t][0], v1 = kKuhn[t][1], v2 = kKuhn[t][2], v3 = kKuhn[t][3];
-          double e1[3], e2[3], e3[3];
-#pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            e1[d] = P[v1][d] - P[v0][d];
-            e2[d] = P[v2][d] - P[v0][d];
-            e3[d] = P[v3][d] - P[v0][d];
-          }
-          const double c1[3] = {e2[1] * e3[2] - e2[2] * e3[1], e2[2] * e3[0] - e2[0] * e3[2],
-                                e2[0] * e3[1] - e2[1] * e3[0]};
-          const double c2[3] = {e3[1] * e1[2] - e3[2] * e1[1], e3[2] * e1[0] - e3[0] * e1[2],
-                                e3[0] * e1[1] - e3[1] * e1[0]};
-          const double c3[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2],
-                                e1[0] * e2[1] - e1[1] * e2[0]};
-          const double det = e1[0] * c1[0] + e1[1] * c1[1] + e1[2] * c1[2];
-          const double du1 = U[v1] - U[v0], du2 = U[v2] - U[v0], du3 = U[v3] - U[v0];
-          double G[3];
-#pragma unroll
-          for (int d = 0; d < 3; ++d) G[d] = fma(c1[d], du1, fma(c2[d], du2, c3[d] * du3));
-          const double s = 1.0 / (6.0 * fabs(det));
-          const double y1 = fma(c1[0], G[0], fma(c1[1], G[1], c1[2] * G[2])) * s;
-          const double y2 = fma(c2[0], G[0], fma(c2[1], G[1], c2[2] * G[2])) * s;
-          const double y3 = fma(c3[0], G[0], fma(c3[1], G[1], c3[2] * G[2])) * s;
-          yc[v1] += y1;
-          yc[v2] += y2;
-          yc[v3] += y3;
-          yc[v0] -= (y1 + y2) + y3;  // rows of K_T sum to zero
-        }
-      }
+      if (k0 <= an_lim) cube(an_o, an_tm, P0, P1, U0, U1, yc);
 #pragma unroll
       for (int c = 0; c < 4; ++c) sm.bot[c * slot_len + oa] = yc[c];
 #pragma unroll
       for (int c = 0; c < 4; ++c) topb[c * slot_len + oa] = yc[4 + c];
+    }
+    // the last band also owns the cubes anchored on diagonal N-1 (slab 0 only):
+    // of their tets only YZX, ZXY, ZYX reach interior nodes (corners 4, 6 on
+    // diagonal N-2, plane 1); corners 1, 3 would lie on diagonal N
+    if (k0 == 0 && bi == n_bands - 1) {
+      for (int x = threadIdx.x; x < N; x += blockDim.x) {
+        int lim, o[8];
+        uint8_t tm;
+        const int col = (int)col_idx(x, N - 1 - x);
+        anchor_setup(col, lim, tm, o);
+        double yc[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) yc[c] = 0.0;
+        cube(o, tm, P0, P1, U0, U1, yc);
+        topb[col - clo] = yc[4];
+        topb[2 * slot_len + col - clo] = yc[6];
+      }
     }
   };
 

@@ -166,6 +166,8 @@ struct Level {
   int slot_len = 0;
   std::vector<Band> bands_s;
   Band* d_bands_s = nullptr;
+  std::vector<Band> bands_fem;  // element-wise FEM: <= kMarchThreads anchor columns per band
+  Band* d_bands_fem = nullptr;
   int slot_len_s = 0;
   int* d_gs_flags_s = nullptr;
   // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order

@@ -532,7 +532,7 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
   if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !force_v1() && !lv.bands.empty() && fem_kernel == 0) {
     // plane range per band (the first band's also holds diagonal 0)
     int need = 0;
-    for (const Band& bb : lv.bands) need = std::max(need, bb.ncols + (bb.d0 == 2 ? bb.c_lo : 0));
+    for (const Band& bb : lv.bands_fem) need = std::max(need, bb.ncols + (bb.d0 == 2 ? bb.c_lo : 0));
     const int slot = std::max(lv.slot_len, (need + 3 + 3) / 4 * 4);
     const size_t smem = ew_smem_bytes(slot, lv.N);
     if (need + 1 > kFPosPerThread * kMarchThreads || smem > (size_t)kMaxDynSmem)
@@ -547,24 +547,24 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
       HHG_CK(c, cudaMalloc(&lv.d_ew_lo, lv.n_local * sizeof(double)));
       HHG_CK(c, cudaMalloc(&lv.d_ew_hi, lv.n_local * sizeof(double)));
     }
-    const int nb = (int)lv.bands.size();
+    const int nb = (int)lv.bands_fem.size();
     ProfScope ps(c, 0);
     const unsigned grid = (unsigned)(nb * c->nt_local);
     if (mode == kModeApply)
-      k_vol_fem_ew<kModeApply><<<grid, kMarchThreads, smem, c->stream>>>(lv.N, lv.S, lv.d_bands, nb, slot, c->d_geo,
-                                                                         c->blended, u, f, out, lv.d_ew_lo, lv.d_ew_hi);
+      k_vol_fem_ew<kModeApply><<<grid, kMarchThreads, smem, c->stream>>>(
+          lv.N, lv.S, lv.d_bands_fem, nb, slot, c->d_geo, c->blended, u, f, out, lv.d_ew_lo, lv.d_ew_hi);
     else
-      k_vol_fem_ew<kModeResid><<<grid, kMarchThreads, smem, c->stream>>>(lv.N, lv.S, lv.d_bands, nb, slot, c->d_geo,
-                                                                         c->blended, u, f, out, lv.d_ew_lo, lv.d_ew_hi);
+      k_vol_fem_ew<kModeResid><<<grid, kMarchThreads, smem, c->stream>>>(
+          lv.N, lv.S, lv.d_bands_fem, nb, slot, c->d_geo, c->blended, u, f, out, lv.d_ew_lo, lv.d_ew_hi);
     HHG_LAUNCHED(c);
     if (nb > 1) {
       int maxcol = 0;
-      for (const Band& bb : lv.bands) maxcol = std::max(maxcol, bb.d1 + bb.d0);
+      for (const Band& bb : lv.bands_fem) maxcol = std::max(maxcol, bb.d1 + bb.d0);
       const dim3 fg(nblk((int64_t)maxcol * (lv.N - 1), 128), (unsigned)c->nt_local, (unsigned)nb);
       if (mode == kModeApply)
-        k_fem_ew_fixup<kModeApply><<<fg, 128, 0, c->stream>>>(lv.N, lv.S, lv.d_bands, nb, lv.d_ew_lo, lv.d_ew_hi, out);
+        k_fem_ew_fixup<kModeApply><<<fg, 128, 0, c->stream>>>(lv.N, lv.S, lv.d_bands_fem, nb, lv.d_ew_lo, lv.d_ew_hi, out);
       else
-        k_fem_ew_fixup<kModeResid><<<fg, 128, 0, c->stream>>>(lv.N, lv.S, lv.d_bands, nb, lv.d_ew_lo, lv.d_ew_hi, out);
+        k_fem_ew_fixup<kModeResid><<<fg, 128, 0, c->stream>>>(lv.N, lv.S, lv.d_bands_fem, nb, lv.d_ew_lo, lv.d_ew_hi, out);
       HHG_LAUNCHED(c);
     }
     return HHG_OK;

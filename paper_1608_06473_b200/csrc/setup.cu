@@ -226,6 +226,22 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if (!make_bands(kMarchThreads, lv.bands, lv.slot_len))
     return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA");
   if (!make_bands(kNarrowThreads, lv.bands_s, lv.slot_len_s)) lv.bands_s.clear();  // N > 129: not used
+  // element-wise FEM bands: <= kMarchThreads ANCHOR columns (every column of a
+  // diagonal, d+1; the first band also anchors diagonal 1's 2 columns)
+  lv.bands_fem.clear();
+  for (int d = 2; d <= N - 2;) {
+    Band b{};
+    b.d0 = d;
+    int cnt = d == 2 ? 2 : 0, ni = 0;
+    while (d <= N - 2 && cnt + (d + 1) <= kMarchThreads) cnt += d + 1, ni += d - 1, ++d;
+    if (d == b.d0) return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA (fem bands)");
+    b.d1 = d;
+    b.ncolumns = ni;
+    b.c_lo = (int)col_idx(b.d0 - 1, 0);
+    b.ncols = (int)col_idx(0, b.d1) + 1 - b.c_lo;
+    b.kmax = N - 1 - b.d0;
+    lv.bands_fem.push_back(b);
+  }
   lv.n_local = lv.S * c->nt_blocks;
   GidInfo& g = lv.gi;
   g.N = N;
@@ -535,6 +551,7 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
   if ((st = up(lv.d_bands, lv.bands)) != HHG_OK) return st;
   if ((st = up(lv.d_bands_s, lv.bands_s)) != HHG_OK) return st;
+  if ((st = up(lv.d_bands_fem, lv.bands_fem)) != HHG_OK) return st;
   {
     const size_t nfl = (size_t)c->nt_local * std::max<size_t>(lv.bands.size(), 1) * 4;
     HHG_CK(c, cudaMalloc(&lv.d_gs_flags, nfl * sizeof(int)));
@@ -567,7 +584,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();

@@ -1,6 +1,6 @@
 """Small driver for ncu captures: one ctx, a few calls of one operation.
 
-usage: python tools/prof_run.py [apply|resid|gs|const] [t] [n_r] [L] [reps]
+usage: python tools/prof_run.py [apply|resid|gs|const|fem] [t] [n_r] [L] [reps]
 """
 import os
 import sys
@@ -34,6 +34,8 @@ def main():
             ctx.apply(L, u, y)
         elif what == "const":
             ctx.apply(L, u, y, op="const")
+        elif what == "fem":
+            ctx.apply(L, u, y, op="fem")
         elif what == "resid":
             ctx.residual(L, u, f, y)
         elif what == "gs":
