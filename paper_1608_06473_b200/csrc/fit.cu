@@ -117,6 +117,11 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
   if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context");
   if (q < 0 || q > 4) return set_err(c, HHG_ERR_INVALID, "q must be in 0..4 (PAPER.md:530-534)");
   if (method != HHG_FIT_LSQP && method != HHG_FIT_IPOLY) return set_err(c, HHG_ERR_INVALID, "method");
+  if (c->vc_graph) {  // a cached V-cycle graph holds the old coefficient buffers
+    cudaStreamSynchronize(c->stream);
+    cudaGraphExecDestroy(c->vc_graph);
+    c->vc_graph = nullptr;
+  }
   if (method == HHG_FIT_IPOLY && q != 2)
     return set_err(c, HHG_ERR_INVALID, "IPOLY points are defined for q = 2 (PAPER.md:490-499)");
   const int mq = n_coeffs(q);

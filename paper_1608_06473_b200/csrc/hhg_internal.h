@@ -212,6 +212,11 @@ struct Ctx {
   std::string err;
   bool poisoned = false;
   cudaStream_t stream = nullptr;
+  cudaStream_t cap_stream = nullptr;  // graph capture (the ctx stream may be the legacy default stream)
+  // cached V-cycle graph (hhg_vcycle): replayed while the call signature matches
+  cudaGraphExec_t vc_graph = nullptr;
+  int64_t vc_graph_launches = 0;
+  std::vector<int64_t> vc_graph_key;
   int rank = 0, nranks = 1;
   int L_max = 0;
   // nt_local macros owned by this rank are blocks [0, nt_local); ghost macros

@@ -431,11 +431,10 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
     const char* e = getenv("HHG_GS_DEPS");
     gated = (e && std::string(e) == "gate") ? 1 : 0;
   }
-  if (gated && lv.gs_epoch >= 200000) {  // progress words encode epoch * 8192
-    HHG_CK(c, cudaMemsetAsync(flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
-    lv.gs_epoch = 0;
-  }
-  lv.gs_epoch += 1;
+  // completion flags cleared per sweep (epoch 1): the launch is replayable from
+  // a CUDA graph (hhg_vcycle)
+  HHG_CK(c, cudaMemsetAsync(flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
+  lv.gs_epoch = 1;
   HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
   const int64_t items = c->nt_local * nb;
   ProfScope ps(c, 1);

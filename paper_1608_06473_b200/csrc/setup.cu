@@ -861,6 +861,8 @@ extern "C" void hhg_destroy(hhg_ctx ctx) {
   if (c->d_cg) cudaFree(c->d_cg);
   if (c->d_scal) cudaFree(c->d_scal);
   if (c->d_own) cudaFree(c->d_own);
+  if (c->vc_graph) cudaGraphExecDestroy(c->vc_graph);
+  if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   for (auto& v : c->ev_rec)
     for (auto& p : v) {

@@ -14,6 +14,7 @@
 // the owner through dist_sum_to_owner (the reverse of the ghost sync), and
 // prolongation re-syncs the ghost slots it cannot compute.
 #include <cmath>
+#include <cstdlib>
 
 #include "fem_device.cuh"
 #include "hhg_internal.h"
@@ -265,8 +266,57 @@ extern "C" hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coa
     res_hist[0] = nr;
     prev = nr;
   }
+  // Cycles after the first (which allocates the level vectors and sizes the
+  // persistent grids) replay one captured CUDA graph: the coarse levels are
+  // launch-bound (~900 launches per cycle).  Not with the host transport
+  // (host callbacks), while profiling, or with the experimental GS variants.
+  bool use_graph = c->transport != 2 && !c->prof && !getenv("HHG_NO_GRAPH") && !getenv("HHG_GS_DEPS") &&
+                   !getenv("HHG_GS_KERNEL");
+  // the graph is cached on the ctx and reused by later calls with the same
+  // signature (levels, smoother, vectors)
+  const std::vector<int64_t> key = {L, L_coarse, nu1, nu2, coarse_cg_iters, (int64_t)op, (int64_t)(intptr_t)du,
+                                    (int64_t)(intptr_t)df};
+  if (c->vc_graph && c->vc_graph_key != key) {
+    cudaGraphExecDestroy(c->vc_graph);
+    c->vc_graph = nullptr;
+  }
+  cudaGraphExec_t& gexec = c->vc_graph;
+  int64_t& graph_launches = c->vc_graph_launches;
   for (int cyc = 0; cyc < n_cycles; ++cyc) {
-    if ((st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, du, df)) != HHG_OK) return st;
+    if ((cyc == 0 && !gexec) || !use_graph) {
+      if ((st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, du, df)) != HHG_OK) return st;
+    } else {
+      if (!gexec) {
+        cudaGraph_t graph = nullptr;
+        const int64_t l0 = c->launches;
+        // capture on a private stream (the legacy default stream cannot be
+        // captured); nothing executes during capture, the replay goes to c->stream
+        if (!c->cap_stream) HHG_CK(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        cudaStream_t orig = c->stream;
+        c->stream = c->cap_stream;
+        const cudaError_t eb = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+        if (eb != cudaSuccess) {
+          c->stream = orig;
+          HHG_CK(c, eb);
+        }
+        st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, du, df);
+        const cudaError_t ee = cudaStreamEndCapture(c->stream, &graph);
+        c->stream = orig;
+        if (st != HHG_OK) {
+          if (graph) cudaGraphDestroy(graph);
+          return st;
+        }
+        HHG_CK(c, ee);
+        graph_launches = c->launches - l0;
+        c->launches = l0;
+        const cudaError_t ei = cudaGraphInstantiate(&gexec, graph, 0);
+        cudaGraphDestroy(graph);
+        HHG_CK(c, ei);
+        c->vc_graph_key = key;
+      }
+      HHG_CK(c, cudaGraphLaunch(gexec, c->stream));
+      c->launches += graph_launches;
+    }
     if (res_hist) {
       if ((st = resnorm(&nr)) != HHG_OK) return st;
       res_hist[cyc + 1] = nr;
