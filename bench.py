@@ -335,6 +335,8 @@ def main():
         if rank == 0:
             out["e2e"] = ee
             out["comparisons"] = cmp
+            if ws == 1:
+                out["comparisons"].update(other_configs(stream, q))
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(L, q)
     if rank == 0:
@@ -398,6 +400,52 @@ def comparisons(ctx, L, u, f, y, n_owned, tmax):
     res["vcycle_V33"] = {"ms_per_cycle": tmax(e0.elapsed_time(e1) / ncyc), "levels": f"2..{L}",
                          "residual_history": [float(h) for h in hist],
                          "reduction_per_cycle": [float(r) for r in rates]}
+    return res
+
+
+def other_configs(stream, q):
+    """BASELINE configs 2 and 3 as context lines (1 GPU): config 2 = the single
+    curved tet at L = 7 (333,375 unknowns, 2.7 MB per vector: L2-resident and
+    launch-bound, reported as-is), apply + 1 GS sweep per step; config 3 = the
+    480-macro shell at L = 6 (20.8 M unknowns), residual + 2 GS sweeps per step."""
+    import numpy as np
+    import torch
+
+    import paper_1608_06473_b200 as hhg
+    import synth
+    res = {}
+    for name, mesh, L, kind in (("config2_single_tet_L7", synth.single_tet(), 7, "apply+gs"),
+                                ("config3_shell480_L6", synth.shell_mesh(0.55, 1.0, 1, 2), 6, "resid+2gs")):
+        ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream)
+        ctx.fit(q, "lsqp", 2)
+        n_local, n_owned, n_global = ctx.layout(L)
+        g = np.arange(n_global, dtype=np.int64)
+        u, f, y = ctx.zeros(L), ctx.zeros(L), ctx.zeros(L)
+        ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(0, g)).cuda(), u)
+        ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(1, g)).cuda(), f)
+
+        def step():
+            if kind == "apply+gs":
+                ctx.apply(L, u, y)
+                ctx.gs_sweep(L, u, f, 1)
+            else:
+                ctx.residual(L, u, f, y)
+                ctx.gs_sweep(L, u, f, 2)
+        for _ in range(3):
+            step()
+        torch.cuda.synchronize()
+        reps = 20
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        lups = (2 if kind == "apply+gs" else 3) * n_owned
+        res[name] = {"step": kind, "unknowns": n_owned, "ms_per_step": ms, "glups": lups / (ms * 1e-3) / 1e9,
+                     "note": "L2-resident, launch-bound" if n_owned < 1e6 else "inputs larger than L2"}
+        ctx.close()
     return res
 
 

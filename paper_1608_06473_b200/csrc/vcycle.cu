@@ -266,11 +266,16 @@ extern "C" hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coa
     res_hist[0] = nr;
     prev = nr;
   }
-  // Cycles after the first (which allocates the level vectors and sizes the
-  // persistent grids) replay one captured CUDA graph: the coarse levels are
-  // launch-bound (~900 launches per cycle).  Not with the host transport
-  // (host callbacks), while profiling, or with the experimental GS variants.
-  bool use_graph = c->transport != 2 && !c->prof && !getenv("HHG_NO_GRAPH") && !getenv("HHG_GS_DEPS") &&
+  // HHG_VCYCLE_GRAPH=1: cycles after the first (which allocates the level
+  // vectors and sizes the persistent grids) replay one captured CUDA graph,
+  // cached on the ctx for later calls with the same signature.  Measured on the
+  // 480-macro L = 7 shell: a replay saves ~2 ms of launch overhead per cycle
+  // (coarse levels 4.0 -> 2.6 ms), but capture + instantiation of the ~1050
+  // nodes costs ~130 ms, so it pays only across many calls -- off by default.
+  // Never with the host transport (host callbacks), while profiling, or with
+  // the experimental GS variants.
+  const char* ge = getenv("HHG_VCYCLE_GRAPH");
+  bool use_graph = ge && atoi(ge) == 1 && c->transport != 2 && !c->prof && !getenv("HHG_GS_DEPS") &&
                    !getenv("HHG_GS_KERNEL");
   // the graph is cached on the ctx and reused by later calls with the same
   // signature (levels, smoother, vectors)

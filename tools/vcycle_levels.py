@@ -37,7 +37,7 @@ for Lt in range(3, L + 1):
     parts = " ".join(f"{k}={v[0] / 2:.2f}" for k, v in prof.items() if v[1])
     tprof = e0.elapsed_time(e1) / 2
     lpc = (ctx.kernel_launches - l0) / 2
-    ctx.vcycle(Lt, u, f, n_cycles=2)  # unprofiled: captures the graph
+    ctx.vcycle(Lt, u, f, n_cycles=2)  # unprofiled (HHG_VCYCLE_GRAPH=1: captures the graph)
     e0.record()
     ctx.vcycle(Lt, u, f, n_cycles=3)  # replays the cached graph
     e1.record()
