@@ -208,9 +208,9 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
                 const double* __restrict__ u, const double* __restrict__ f, double* __restrict__ out, int T0) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem<> sm(smem, slot_len);
-  const int Tl = blockIdx.x / n_bands;  // macro within the launch chunk (uniform)
+  const int Tl = blockIdx.y;  // macro within the launch chunk (uniform: S2UR)
   const int64_t T = T0 + Tl;
-  const Band b = bands[blockIdx.x - Tl * n_bands];
+  const Band b = bands[blockIdx.x];
   const double* ub = u + T * S;
   // barriers + plane offsets, then the first kRing planes are put in flight
   // BEFORE the column coefficients are computed (their HBM latency overlaps it)
@@ -422,7 +422,8 @@ template <int OP, int RING, class Gate = NoGate>
 __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_len, int N, const Band& b,
                                                  const Column& q, const double (&A)[15], const double (&B)[15],
                                                  int colour, double* __restrict__ ub, const double* __restrict__ fb,
-                                                 double* __restrict__ wb, const Gate& gate = Gate()) {
+                                                 double* __restrict__ wb, const double* __restrict__ Cw,
+                                                 const Gate& gate = Gate()) {
   constexpr int NQ = RING / 4;
 #ifdef HHG_GS_PROF
   long long _tp0 = clock64();
@@ -486,7 +487,7 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
     if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
     if (q.active && k >= 1 && k <= q.len) {
       const double kd = (double)k;
-      const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(sm.Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
+      const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
       const double rinv = rcp_nr(smc);
       const double* Pb = sptr(k - 1);
       const double* Pm = sptr(k);
@@ -502,7 +503,7 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
           if (w == kMC) continue;
           x = fma(A[w], uu[w], x);
           y = fma(B[w], uu[w], y);
-          z = fma(sm.Cw[w], uu[w], z);
+          z = fma(Cw[w], uu[w], z);
         }
         r = fma(fma(z, kd, y), kd, x);
       } else {
@@ -578,28 +579,40 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // running yet; every other running item's neighbours run too => no deadlock
 // while the grid has more CTAs than a macro has bands.
 // ---------------------------------------------------------------------------
-template <int OP, int NT, int RING>
+// ST (static schedule, default): CTA x takes items x, x + grid, x + 2 grid, ...
+// of the launch's macro chunk [T0, T0 + ntl), so the item -- and the macro's 15
+// C_w in the constant bank (g_cC, uploaded per chunk) -- are uniform: they sit
+// in uniform registers as DFMA operands.  Deadlock-free with every CTA
+// resident: pass c of item j waits only on items j +- 1 at pass c-1, so the
+// items of a wave finish their first passes without the next wave and at
+// least grid - 3 CTAs of a wave complete and move on.  !ST: items from an
+// atomic counter, C_w through shared memory.
+template <int OP, int NT, int RING, bool ST>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
-               const double* __restrict__ f, int64_t ntl, int G, int* __restrict__ counter,
+               const double* __restrict__ f, int64_t ntl, int T0, int* __restrict__ counter,
                int* __restrict__ flags, int epoch) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem<RING> sm(smem, slot_len);
   __shared__ int s_item;
-  (void)G;
   const int64_t total = ntl * n_bands;
 #ifdef HHG_GS_PROF
   if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)(-clock64()));
 #endif
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
-    __syncthreads();
-    const int64_t item = s_item;
-    __syncthreads();
+  for (int64_t it = blockIdx.x;; it += gridDim.x) {
+    int64_t item = it;
+    if (!ST) {
+      if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
+      __syncthreads();
+      item = s_item;
+      __syncthreads();
+    }
     if (item >= total) break;
-    const int64_t T = item / n_bands;
-    const int band = (int)(item - T * n_bands);
+    const int Tl = (int)(item / n_bands);
+    const int64_t T = T0 + Tl;
+    const int band = (int)(item - (int64_t)Tl * n_bands);
+    const double* const Cw = ST ? g_cC + Tl * 15 : sm.Cw;
     const Band b = bands[band];
     Column q;
     double A[15], B[15];
@@ -627,7 +640,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         GPROF_T0
         if (RING % 8 == 0 && RING >= 24)
           gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
-                                     u + T * S + q.c);
+                                     u + T * S + q.c, Cw);
         else
           gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
         {

@@ -266,7 +266,7 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
     if (OP == HHG_OP_SURROGATE)
       HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
                                         cudaMemcpyDeviceToDevice, c->stream));
-    k_vol_march<OP, MODE><<<(unsigned)(nb * nt), kMarchThreads, smem, c->stream>>>(
+    k_vol_march<OP, MODE><<<dim3((unsigned)nb, (unsigned)nt), kMarchThreads, smem, c->stream>>>(
         lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, (int)T0);
     HHG_LAUNCHED(c);
   }
@@ -404,11 +404,12 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
   static std::map<size_t, int> grids;
   int& grid = grids[smem];
   if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
     int dev = 0, sms = 0, per_sm = 0;
     HHG_CK(c, cudaGetDevice(&dev));
     HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT, RING>, NT, smem));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT, RING, true>, NT, smem));
     grid = sms * std::max(per_sm, 1);
   }
   const int nb = (int)bands.size();
@@ -449,11 +450,36 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
         lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter, flags,
         lv.gs_epoch);
   } else {
-    k_gs_items<OP, NT, RING><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
-        lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, G, lv.d_gs_counter, flags,
-        lv.gs_epoch);
+    // default: items from an atomic counter, C_w in shared memory;
+    // HHG_GS_SCHED=static: round-robin items, C_w in uniform registers (measured
+    // slower: 3.74 vs 3.05 ms, the static mix of long and short bands per CTA)
+    static int dyn = -1;
+    if (dyn < 0) {
+      const char* e = getenv("HHG_GS_SCHED");
+      dyn = (e && std::string(e) == "static") ? 0 : 1;
+    }
+    (void)G;
+    if (dyn) {
+      k_gs_items<OP, NT, RING, false><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+          lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, 0, lv.d_gs_counter, flags,
+          lv.gs_epoch);
+      HHG_LAUNCHED(c);
+    } else {
+      hhg_status st = ensure_cC(c, lv, OP);
+      if (st != HHG_OK) return st;
+      // macro chunks of <= kCMax (the constant-bank C_w table); chunks run in order
+      for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
+        const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
+        if (OP == HHG_OP_SURROGATE)
+          HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
+                                            cudaMemcpyDeviceToDevice, c->stream));
+        k_gs_items<OP, NT, RING, true><<<(unsigned)std::min<int64_t>(grid, nt * nb), NT, smem, c->stream>>>(
+            lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, nt, (int)T0, lv.d_gs_counter, flags,
+            lv.gs_epoch);
+        HHG_LAUNCHED(c);
+      }
+    }
   }
-  HHG_LAUNCHED(c);
   return HHG_OK;
 }
 
