@@ -135,21 +135,29 @@ class Hierarchy:
         m = sp.diags(mask(self.num[L_coarse]))
         self.A_coarse = (m @ self.L[L_coarse] @ m).tocsr()
 
-    def vcycle(self, L, u, f, nu1=3, nu2=3, cg_iters=50):
+    def _res_op(self, L, dd):
+        # double discretisation: the surrogate L~ smooths,
+        # the exact operator L computes the residuals
+        return self.L[L] if dd else self.Lt[L]
+
+    def vcycle(self, L, u, f, nu1=3, nu2=3, cg_iters=50, dd=False):
         if L == self.L_coarse:
             m = mask(self.num[L])
             return m * cg(self.A_coarse, m * f, cg_iters)
         u = self.gs[L].sweep(u, f, nu1)
-        r = residual(self.Lt[L], self.num[L], u, f)
+        r = residual(self._res_op(L, dd), self.num[L], u, f)
         fc = self.P[L].T @ r
-        uc = self.vcycle(L - 1, np.zeros_like(fc), fc, nu1, nu2, cg_iters)
+        uc = self.vcycle(L - 1, np.zeros_like(fc), fc, nu1, nu2, cg_iters, dd)
         u = u + self.P[L] @ uc
         return self.gs[L].sweep(u, f, nu2)
 
-    def solve(self, u, f, n_cycles, nu1=3, nu2=3, cg_iters=50):
+    def solve(self, u, f, n_cycles, nu1=3, nu2=3, cg_iters=50, dd=False):
+        """n_cycles V(nu1, nu2) cycles; history = ||f - A u||_2 after each, A
+        the residual operator (L~, or L with double discretisation)."""
         L = self.L_max
-        hist = [np.linalg.norm(residual(self.Lt[L], self.num[L], u, f))]
+        A = self._res_op(L, dd)
+        hist = [np.linalg.norm(residual(A, self.num[L], u, f))]
         for _ in range(n_cycles):
-            u = self.vcycle(L, u, f, nu1, nu2, cg_iters)
-            hist.append(np.linalg.norm(residual(self.Lt[L], self.num[L], u, f)))
+            u = self.vcycle(L, u, f, nu1, nu2, cg_iters, dd)
+            hist.append(np.linalg.norm(residual(A, self.num[L], u, f)))
         return u, np.array(hist)

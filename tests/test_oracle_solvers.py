@@ -150,3 +150,34 @@ def test_cg_matches_scipy_and_vcycle_contracts():
     u, hist = H.solve(u0, f, 6)
     rates = hist[1:] / hist[:-1]
     assert np.all(rates[2:] < 0.5), rates
+
+
+def test_double_discretisation_special_cases():
+    """Double discretisation (surrogate smoother, exact
+    residual).  Pins: on an affine macro mesh the surrogate IS the exact
+    operator, so the DD cycle equals the plain cycle; zero
+    data stays zero; on the curved shell the DD history is the exact-operator
+    residual of the DD iterate."""
+    m = synth.shell_mesh(0.55, 1.0, 0, 1)
+    flat = synth.MacroMesh(m.vertices, None, m.tets, m.dirichlet)
+    H = solvers.Hierarchy(flat, 4, 2, 2)
+    num = H.num[4]
+    g = np.arange(num.n_total)
+    f = synth.uniform_pm1(4, g) * num.unknown_mask
+    u0 = synth.uniform_pm1(7, g) * num.unknown_mask
+    u1, h1 = H.solve(u0.copy(), f, 3)
+    u2, h2 = H.solve(u0.copy(), f, 3, dd=True)
+    assert np.abs(h1 - h2).max() <= 1e-11 * h1[0]
+    assert np.linalg.norm(u1 - u2) <= 1e-11 * np.linalg.norm(u1)
+    z = np.zeros(num.n_total)
+    uz, hz = H.solve(z.copy(), z, 1, dd=True)
+    assert np.all(uz == 0) and np.all(hz == 0)
+    Hc = solvers.Hierarchy(m, 4, 2, 2)
+    numc = Hc.num[4]
+    A = fem.assemble(m, 16, numc, blended=True)
+    fc = synth.uniform_pm1(4, np.arange(numc.n_total)) * numc.unknown_mask
+    uc0 = synth.uniform_pm1(7, np.arange(numc.n_total)) * numc.unknown_mask
+    uc, hc = Hc.solve(uc0.copy(), fc, 2, dd=True)
+    mk = numc.unknown_mask
+    assert abs(hc[-1] - np.linalg.norm(mk * (fc - A @ (mk * uc)))) <= 1e-12 * hc[0]
+    assert hc[-1] < 0.5 * hc[0]
