@@ -400,6 +400,15 @@ def comparisons(ctx, L, u, f, y, n_owned, tmax):
     res["vcycle_V33"] = {"ms_per_cycle": tmax(e0.elapsed_time(e1) / ncyc), "levels": f"2..{L}",
                          "residual_history": [float(h) for h in hist],
                          "reduction_per_cycle": [float(r) for r in rates]}
+    # double discretisation: surrogate smoother, element-wise
+    # FEM residual on every level; history = exact-operator residual
+    uu.copy_(u)
+    e0.record()
+    hist = ctx.vcycle(L, uu, ff, n_cycles=ncyc, residual_op="fem")
+    e1.record()
+    torch.cuda.synchronize()
+    res["vcycle_V33_DD"] = {"ms_per_cycle": tmax(e0.elapsed_time(e1) / ncyc), "levels": f"2..{L}",
+                            "residual_history": [float(h) for h in hist]}
     return res
 
 

@@ -156,6 +156,16 @@ hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, const double* 
 hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
                       hhg_op op, double* u, const double* f, int n_cycles, double* res_hist);
 
+/* Double discretisation: as hhg_vcycle, but the residuals
+ * on every level -- and res_hist -- use residual_op (e.g. FEM_ELEMENTWISE, the
+ * exact operator) while smoother_op (SURROGATE or CONST_AFFINE) smooths.  The
+ * two operators pull towards different algebraic solutions,
+ * so the history is not expected to decrease to zero.  residual_op ==
+ * smoother_op is hhg_vcycle.  HHG_ERR_INVALID for an unknown residual_op. */
+hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
+                         hhg_op smoother_op, hhg_op residual_op, double* u, const double* f, int n_cycles,
+                         double* res_hist);
+
 /* Canonical global vector (length n_global_nodes, DESIGN.md numbering:
  * vertices, edges, faces, volumes) <-> local layout.  gather writes every
  * node (0 at Dirichlet); scatter writes every copy and zeroes Dirichlet slots.

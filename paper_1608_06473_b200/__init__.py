@@ -46,6 +46,7 @@ def lib():
     L.hhg_residual.argtypes = [P, I32, I32, P, P, P, P]
     L.hhg_gs_sweep.argtypes = [P, I32, I32, P, P, I32]
     L.hhg_vcycle.argtypes = [P, I32, I32, I32, I32, I32, I32, P, P, I32, P]
+    L.hhg_vcycle_dd.argtypes = [P, I32, I32, I32, I32, I32, I32, I32, P, P, I32, P]
     L.hhg_gather_global.argtypes = [P, I32, P, P]
     L.hhg_scatter_global.argtypes = [P, I32, P, P]
     L.hhg_sync_copies.argtypes = [P, I32, P]
@@ -66,7 +67,7 @@ def lib():
     L.hhg_last_error.restype = ctypes.c_char_p
     L.hhg_destroy.argtypes = [P]
     for name in ("hhg_setup_macro_mesh", "hhg_fit_surrogates", "hhg_vector_layout", "hhg_apply",
-                 "hhg_residual", "hhg_gs_sweep", "hhg_vcycle", "hhg_gather_global",
+                 "hhg_residual", "hhg_gs_sweep", "hhg_vcycle", "hhg_vcycle_dd", "hhg_gather_global",
                  "hhg_scatter_global", "hhg_sync_copies", "hhg_eval_stencils"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
@@ -226,11 +227,17 @@ class Ctx:
         self._check(self._lib.hhg_gs_sweep(self.h, L, OPS[op], _ptr(u, n), _ptr(f, n), n_sweeps))
         return u
 
-    def vcycle(self, L, u, f, n_cycles=1, nu1=3, nu2=3, L_coarse=2, cg_iters=50, op="surrogate"):
+    def vcycle(self, L, u, f, n_cycles=1, nu1=3, nu2=3, L_coarse=2, cg_iters=50, op="surrogate", residual_op=None):
+        """V(nu1,nu2) cycles in place on u; residual_op (e.g. "fem") selects
+        double discretisation (hhg_vcycle_dd)."""
         n = self.layout(L)[0]
         hist = np.zeros(n_cycles + 1)
-        self._check(self._lib.hhg_vcycle(self.h, L, nu1, nu2, L_coarse, cg_iters, OPS[op], _ptr(u, n),
-                                         _ptr(f, n), n_cycles, hist.ctypes.data))
+        if residual_op is None:
+            self._check(self._lib.hhg_vcycle(self.h, L, nu1, nu2, L_coarse, cg_iters, OPS[op], _ptr(u, n),
+                                             _ptr(f, n), n_cycles, hist.ctypes.data))
+        else:
+            self._check(self._lib.hhg_vcycle_dd(self.h, L, nu1, nu2, L_coarse, cg_iters, OPS[op], OPS[residual_op],
+                                                _ptr(u, n), _ptr(f, n), n_cycles, hist.ctypes.data))
         return hist
 
     def gather_global(self, L, local, out=None):
