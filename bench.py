@@ -458,6 +458,32 @@ def other_configs(stream, q):
     return res
 
 
+def cpu_baseline_parallel(step, n_unk, sample, seconds=8.0):
+    """The same oracle step run independently by one forked process per core
+    of os.sched_getaffinity(0) (SciPy's SpMV is single-threaded): aggregate
+    throughput of the host, reported beside the 1-core figure."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+
+    def worker():
+        n, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < seconds:
+            step()
+            n += 1
+        q.put((n, time.perf_counter() - t0))
+    procs = [ctx.Process(target=worker) for _ in range(cores)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=seconds * 20 + 120) for _ in procs]
+    for p in procs:
+        p.join()
+    value = sum(2 * n_unk * n / t for n, t in res) / 1e9
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": sample + f", one process per core, {seconds:.0f} s each"}
+
+
 def cpu_baseline(L, q):
     try:
         n_unk, step, sample = oracle_sample(min(L, 7), q, 1)
@@ -469,8 +495,10 @@ def cpu_baseline(L, q):
             step()
             ts.append(time.perf_counter() - t0)
         t = statistics.median(ts)
-        return {"value": 2 * n_unk / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": sample + f", {len(ts)} reps, median"}
+        out = {"value": 2 * n_unk / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": sample + f", {len(ts)} reps, median"}
+        out["all_cores"] = cpu_baseline_parallel(step, n_unk, sample)
+        return out
     except Exception as e:  # pragma: no cover
         return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": f"failed: {e}"}
 
