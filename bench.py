@@ -214,7 +214,7 @@ def main():
         if host_tr:
             ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream, rank=rank, nranks=ws, owner=owner)
         else:
-            nid = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+            nid = [hhg.nccl_unique_id() if rank == 0 else None]  # the library's own NCCL creates the id
             dist.broadcast_object_list(nid, src=0)
             ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream, rank=rank, nranks=ws, owner=owner,
                                     nccl_id=nid[0])

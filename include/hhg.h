@@ -186,6 +186,12 @@ hhg_status hhg_sync_copies(hhg_ctx ctx, int L, double* local);
  * FEM stencils of the blended / affine geometry. */
 hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t macro, double* out);
 
+/* Writes a fresh NCCL unique id (128 bytes, caller-owned buffer) created by
+ * the NCCL library this library is bound to, for rank 0 to broadcast to every
+ * rank before hhg_setup_macro_mesh (so id creation and communicator setup use
+ * the same NCCL build).  HHG_ERR_NCCL on failure. */
+hhg_status hhg_nccl_unique_id(void* out128);
+
 /* Multi-rank transport for contexts set up with nranks > 1 and
  * nccl_unique_id == NULL (tests; production uses NCCL).  fn moves host buffers
  * between all ranks: for every peer p, send_bytes[p] bytes (concatenated in

@@ -66,6 +66,8 @@ def lib():
     L.hhg_last_error.argtypes = [P]
     L.hhg_last_error.restype = ctypes.c_char_p
     L.hhg_destroy.argtypes = [P]
+    L.hhg_nccl_unique_id.argtypes = [P]
+    L.hhg_nccl_unique_id.restype = ctypes.c_int
     for name in ("hhg_setup_macro_mesh", "hhg_fit_surrogates", "hhg_vector_layout", "hhg_apply",
                  "hhg_residual", "hhg_gs_sweep", "hhg_vcycle", "hhg_vcycle_dd", "hhg_gather_global",
                  "hhg_scatter_global", "hhg_sync_copies", "hhg_eval_stencils"):
@@ -97,6 +99,16 @@ def _ptr(x, n=None, writable=False):
 HostExchangeFn = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int64),
                                   ctypes.c_void_p, ctypes.POINTER(ctypes.c_int64), ctypes.c_void_p)
 _keep_alive = []
+
+
+def nccl_unique_id():
+    """128-byte NCCL unique id from the library's own NCCL (rank 0 creates it,
+    every rank passes it to Ctx.from_mesh(..., nccl_id=...))."""
+    buf = ctypes.create_string_buffer(128)
+    st = lib().hhg_nccl_unique_id(buf)
+    if st != 0:
+        raise HHGError(st, "ncclGetUniqueId")
+    return buf.raw
 
 
 def set_torch_transport(host_only=False, group=None):

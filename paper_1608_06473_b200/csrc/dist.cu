@@ -338,6 +338,15 @@ hhg_status dist_allreduce_sum(Ctx* c, double* d_scalar) {
 
 using namespace hhg;
 
+extern "C" hhg_status hhg_nccl_unique_id(void* out128) {
+  if (!out128) return HHG_ERR_INVALID;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return HHG_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id size");
+  std::memcpy(out128, &id, sizeof(id));
+  return HHG_OK;
+}
+
 extern "C" hhg_status hhg_set_host_transport(hhg_host_exchange_fn fn, void* user, int host_only) {
   g_host_fn = (HostFn)fn;
   g_host_user = user;

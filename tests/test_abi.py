@@ -52,3 +52,11 @@ def test_sass_is_sm100a():
     ge.build()
     out = os.popen(f"cuobjdump --list-elf {ge.SO} 2>&1").read()
     assert "sm_100a" in out
+
+
+def test_nccl_unique_id_from_the_library():
+    """hhg_nccl_unique_id: 128 bytes from the library's own NCCL (no GPU
+    needed); fresh ids differ."""
+    import paper_1608_06473_b200 as hhg
+    a, b = hhg.nccl_unique_id(), hhg.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
