@@ -66,6 +66,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -626,10 +636,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       if (threadIdx.x == 0 && colour > 0) {
         for (int bb = band - 1; bb <= band + 1; bb += 2) {
           if (bb < 0 || bb >= n_bands) continue;
-          const volatile int* fl = flags + ((T * n_bands + bb) * 4 + colour - 1);
-          while (*fl != epoch) __nanosleep(32);
+          const int* fl = flags + ((T * n_bands + bb) * 4 + colour - 1);
+          while (ld_acquire_gpu(fl) != epoch) __nanosleep(32);
         }
-        __threadfence();
       }
       __syncthreads();
       // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
@@ -650,11 +659,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
         GPROF_ADD(1)
       }
-      // bar.sync orders every thread's stores before thread 0's gpu-scope fence (cumulative)
-      if (threadIdx.x == 0) {
-        __threadfence();
-        atomicExch(flags + ((T * n_bands + band) * 4 + colour), epoch);
-      }
+      // bar.sync orders every thread's stores before thread 0's gpu-scope
+      // release (cumulative); the neighbours' acquire loads pair with it
+      if (threadIdx.x == 0) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
     }
   }
 #ifdef HHG_GS_PROF
