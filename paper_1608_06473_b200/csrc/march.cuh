@@ -433,16 +433,18 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
                                                  const Column& q, const double (&A)[15], const double (&B)[15],
                                                  int colour, double* __restrict__ ub, const double* __restrict__ fb,
                                                  double* __restrict__ wb, const double* __restrict__ Cw,
-                                                 const Gate& gate = Gate()) {
+                                                 const Gate& gate = Gate(), bool init_bars = true) {
   constexpr int NQ = RING / 4;
 #ifdef HHG_GS_PROF
   long long _tp0 = clock64();
 #endif
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < NQ; ++s) mbar_init(&sm.bars[s], 4);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (init_bars) {  // else the caller initialised them (gs_quad_bars_init) before a CTA barrier
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < NQ; ++s) mbar_init(&sm.bars[s], 4);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
   const int last_plane = b.kmax + 1;
   const int last_quad = last_plane / 4;
@@ -549,6 +551,16 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
   GPROF_ADD(9)
 }
 
+// thread 0: fresh quad barriers for the next colour pass (every thread is past
+// the previous pass's last wait); made visible by the caller's next bar.sync
+template <int RING>
+__device__ __forceinline__ void gs_quad_bars_init(MarchSmem<RING>& sm) {
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RING / 4; ++s) mbar_init(&sm.bars[s], 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+}
+
 template <int OP, int RING = kRing>
 __device__ __forceinline__ void band_setup(MarchSmem<RING>& sm, int N, const Band& b, int64_t T,
                                            const double* __restrict__ coef10, const double* __restrict__ cons,
@@ -631,6 +643,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       band_setup<OP, RING>(sm, N, b, T, coef10, cons, q, A, B);
       GPROF_ADD(4)
     }
+    constexpr bool kQuad = RING % 8 == 0 && RING >= 24;
+    if (kQuad) gs_quad_bars_init(sm);  // visible after the pass-start bar.sync
     for (int colour = 0; colour < 4; ++colour) {
       GPROF_T0
       if (threadIdx.x == 0 && colour > 0) {
@@ -647,9 +661,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       GPROF_ADD(0)
       {
         GPROF_T0
-        if (RING % 8 == 0 && RING >= 24)
+        if (kQuad)
           gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
-                                     u + T * S + q.c, Cw);
+                                     u + T * S + q.c, Cw, NoGate(), false);
         else
           gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
         {
@@ -662,6 +676,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       // bar.sync orders every thread's stores before thread 0's gpu-scope
       // release (cumulative); the neighbours' acquire loads pair with it
       if (threadIdx.x == 0) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
+      if (kQuad && colour < 3) gs_quad_bars_init(sm);
     }
   }
 #ifdef HHG_GS_PROF
