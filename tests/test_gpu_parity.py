@@ -186,6 +186,17 @@ def test_errors_are_reported():
     with pytest.raises(hhg.HHGError) as e:
         hhg.Ctx.from_mesh(wrong_r, 3)
     assert e.value.status == 2
+    ctx.fit(2)
+    f = ctx.zeros(3)
+    with pytest.raises(hhg.HHGError) as e:          # FEM is not a smoother
+        ctx.vcycle(3, u, f, op="fem")
+    assert e.value.status == 1
+    with pytest.raises(hhg.HHGError) as e:          # unknown residual operator
+        ctx._check(ctx._lib.hhg_vcycle_dd(ctx.h, 3, 3, 3, 2, 50, 0, 7, u.data_ptr(), f.data_ptr(), 1, None))
+    assert e.value.status == 1
+    with pytest.raises(hhg.HHGError) as e:          # u and f alias
+        ctx.vcycle(3, u, u)
+    assert e.value.status == 1
 
 
 @functools.lru_cache(maxsize=None)
