@@ -1,0 +1,32 @@
+"""Discretisation-error trends of PAPER.md Sec. 4.1 / Table hHstudy on the
+60-macro synthetic shell, solved through the C-ABI (tools/accuracy_study.py:
+manufactured solution (r - r1)(r - r2) sin(10x) sin(4y) sin(7z), lumped RHS,
+FEM by CG on the exact element-wise operator, surrogates by 10 V(3,3)
+cycles).  Absolute values are unpinned (the paper's macro mesh is unknown);
+the asserted trends are the paper's findings:
+quadratic FEM convergence; the surrogate error follows FEM on coarse levels
+and departs from it (a plateau) on fine ones, later for higher q."""
+import os
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_hHstudy_trends_60_macros():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import accuracy_study as A
+    variants = [("FEM", 0, None), ("LSQP1", 1, "lsqp"), ("LSQP2", 2, "lsqp"), ("LSQP3", 3, "lsqp")]
+    nt, rows = A.study(0, 1, [3, 4, 5], variants)
+    assert nt == 60
+    fem = {L: rows[L]["FEM"] for L in rows}
+    for L in (3, 4):                                   # quadratic FEM convergence
+        assert 3.5 < fem[L] / fem[L + 1] < 4.8, fem
+    for q in ("LSQP1", "LSQP2", "LSQP3"):              # coarse level: surrogate = FEM within 10 %
+        assert abs(rows[3][q] - fem[3]) <= 0.1 * fem[3], (q, rows[3])
+    assert abs(rows[4]["LSQP2"] - fem[4]) <= 0.1 * fem[4]       # q = 2 still on the FEM curve at L = 4
+    assert rows[4]["LSQP1"] > 1.1 * fem[4]                      # q = 1 has left it
+    assert rows[5]["LSQP1"] > rows[5]["LSQP2"] > rows[5]["LSQP3"] > fem[5]   # plateau drops with q
+    assert rows[5]["LSQP1"] > 0.8 * rows[4]["LSQP1"]            # q = 1: no further convergence
