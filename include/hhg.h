@@ -160,8 +160,9 @@ hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int co
  * on every level -- and res_hist -- use residual_op (e.g. FEM_ELEMENTWISE, the
  * exact operator) while smoother_op (SURROGATE or CONST_AFFINE) smooths.  The
  * two operators pull towards different algebraic solutions,
- * so the history is not expected to decrease to zero.  residual_op ==
- * smoother_op is hhg_vcycle.  HHG_ERR_INVALID for an unknown residual_op. */
+ * so the history is not expected to decrease to zero and the growth check of
+ * hhg_vcycle (HHG_ERR_DIVERGED) is off.  residual_op == smoother_op is
+ * hhg_vcycle.  HHG_ERR_INVALID for an unknown residual_op. */
 hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
                          hhg_op smoother_op, hhg_op residual_op, double* u, const double* f, int n_cycles,
                          double* res_hist);

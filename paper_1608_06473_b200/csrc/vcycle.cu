@@ -345,7 +345,9 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
     if (res_hist) {
       if ((st = resnorm(&nr)) != HHG_OK) return st;
       res_hist[cyc + 1] = nr;
-      grow = nr > prev ? grow + 1 : 0;
+      // not for double discretisation: its exact-operator residual stalls and may
+      // creep up by design (residual criteria inappropriate)
+      grow = (nr > prev && rop == op) ? grow + 1 : 0;
       prev = nr;
       if (grow >= 3) {
         result = set_err(c, HHG_ERR_DIVERGED, "V-cycle residual grew three cycles in a row");

@@ -5,7 +5,8 @@ FEM by CG on the exact element-wise operator, surrogates by 10 V(3,3)
 cycles).  Absolute values are unpinned (the paper's macro mesh is unknown);
 the asserted trends are the paper's findings:
 quadratic FEM convergence; the surrogate error follows FEM on coarse levels
-and departs from it (a plateau) on fine ones, later for higher q."""
+and departs from it (a plateau) on fine ones, later for higher q; double
+discretisation recovers the FEM error."""
 import os
 import sys
 
@@ -18,7 +19,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def test_hHstudy_trends_60_macros():
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import accuracy_study as A
-    variants = [("FEM", 0, None), ("LSQP1", 1, "lsqp"), ("LSQP2", 2, "lsqp"), ("LSQP3", 3, "lsqp")]
+    variants = [("FEM", 0, None), ("LSQP1", 1, "lsqp"), ("LSQP2", 2, "lsqp"), ("LSQP3", 3, "lsqp"),
+                ("LSQP2-DD", 2, "lsqp-dd")]
     nt, rows = A.study(0, 1, [3, 4, 5], variants)
     assert nt == 60
     fem = {L: rows[L]["FEM"] for L in rows}
@@ -30,3 +32,6 @@ def test_hHstudy_trends_60_macros():
     assert rows[4]["LSQP1"] > 1.1 * fem[4]                      # q = 1 has left it
     assert rows[5]["LSQP1"] > rows[5]["LSQP2"] > rows[5]["LSQP3"] > fem[5]   # plateau drops with q
     assert rows[5]["LSQP1"] > 0.8 * rows[4]["LSQP1"]            # q = 1: no further convergence
+    # double discretisation (almost) recovers the FEM error
+    for L in (3, 4, 5):
+        assert abs(rows[L]["LSQP2-DD"] - fem[L]) <= 0.1 * fem[L], (L, rows[L])
