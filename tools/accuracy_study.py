@@ -105,7 +105,8 @@ VARIANTS = [("FEM", 0, None), ("LSQP1", 1, "lsqp"), ("LSQP2", 2, "lsqp"), ("LSQP
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else None
     t0 = time.time()
-    tables = [study(0, 1, [2, 3, 4, 5, 6], VARIANTS), study(1, 2, [2, 3, 4, 5], VARIANTS)]
+    tables = [study(0, 1, [2, 3, 4, 5, 6], VARIANTS), study(1, 2, [2, 3, 4, 5], VARIANTS),
+              study(2, 4, [2, 3, 4], VARIANTS)]
     lines = ["# Discretisation error (lumped-mass discrete L2), PAPER.md Table hHstudy setting on the",
              "# synthetic icosahedral shells (parity unpinned: the paper's macro mesh is unknown).",
              "# FEM: CG on the exact element-wise operator; LSQP/IPOLY: 10 V(3,3) cycles (j = 2).",
