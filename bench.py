@@ -145,6 +145,17 @@ def oracle_sample(L, q, n_macros=1):
     return n_unk, step, f"oracle (scipy CSR SpMV + colour-step GS) on {n_macros} macro(s) of the 480-macro shell at L={L}"
 
 
+def workload(a, ws):
+    """(t, n_r, workload string) of the bench configuration at ws GPUs --
+    weak scaling (BASELINE config 4): ~480 macros per GPU;
+    1: t=1 n_r=2 (480), 2: t=1 n_r=4 (960), 4: t=2 n_r=2 (1920), 8: t=2 n_r=4 (3840)."""
+    t, nr = a.t, a.nr
+    if ws > 1 and (a.t, a.nr) == (1, 2):
+        t, nr = {2: (1, 4), 4: (2, 2), 8: (2, 4)}.get(ws, (1, 2 * ws))
+    nt = 60 * 4 ** t * nr
+    return t, nr, f"shell t={t} n_r={nr} ({nt} macros) L={a.L} q={a.q} LSQP j=2, apply + 1 GS sweep"
+
+
 def run_reference(a):
     ws, rank, local = dist_env()
     if rank != 0:
@@ -163,8 +174,7 @@ def run_reference(a):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": a.gpus,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"shell t={a.t} n_r={a.nr} L={a.L} q={a.q} (sampled)",
-                      "sample": sample},
+           "config": {"workload": workload(a, ws)[2], "sample": sample},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -200,11 +210,7 @@ def main():
     rdev = torch.device("cpu") if host_tr else dev  # device of the reduction tensors
     stream = torch.cuda.current_stream(dev)
     L, q = a.L, a.q
-    # weak scaling (BASELINE config 4): ~480 macros per GPU --
-    # 1: t=1 n_r=2 (480), 2: t=1 n_r=4 (960), 4: t=2 n_r=2 (1920), 8: t=2 n_r=4 (3840)
-    t_ref, nr_ref = a.t, a.nr
-    if ws > 1 and (a.t, a.nr) == (1, 2):
-        t_ref, nr_ref = {2: (1, 4), 4: (2, 2), 8: (2, 4)}.get(ws, (1, 2 * ws))
+    t_ref, nr_ref, workload_str = workload(a, ws)
     mesh = synth.shell_mesh(0.55, 1.0, t_ref, nr_ref)
     t0 = time.time()
     if ws > 1:
@@ -308,8 +314,7 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"shell t={t_ref} n_r={nr_ref} ({mesh.nt} macros) L={L} q={q} LSQP j=2, "
-                                  f"apply + 1 GS sweep", "unknowns": n_owned_total,
+           "config": {"workload": workload_str, "unknowns": n_owned_total,
                       "macros_per_gpu": mesh.nt // ws,
                       "parallelism": (f"macro partition over {ws} ranks, "
                                       + ("host (gloo) ghost exchange, ranks sharing a GPU: functional check, "
