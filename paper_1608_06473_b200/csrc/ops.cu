@@ -116,18 +116,32 @@ __device__ inline double block_sum(double v) {
 
 // sum over unique unknowns of a*b: volume interiors + CSR rows at their owner
 // copy (face rows: faces.cu::k_face_dot)
+// sum over the interior volume nodes (column march: thread = (macro, lattice
+// column (i, j)), k = 1 .. N-1-i-j; consecutive threads read consecutive
+// columns of a plane) and the owned lower-primitive rows.  Fixed grid and
+// mapping: deterministic.
 __global__ void k_dot(int N, int64_t S, int64_t P, int64_t ntl, const double* __restrict__ a,
                       const double* __restrict__ b, int64_t n_rows, const uint32_t* __restrict__ lp_owner_col,
                       const uint64_t* __restrict__ rp, double* __restrict__ part) {
+  __shared__ int64_t po_s[258];
+  for (int k = threadIdx.x; k <= N; k += blockDim.x) po_s[k] = plane_off(N, k);
+  __syncthreads();
+  (void)P;
   double acc = 0.0;
-  const int64_t tot = ntl * P;
+  const int64_t ncol = (int64_t)(N + 1) * (N + 2) / 2;  // columns of plane 0
+  const int64_t tot = ntl * ncol;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
        t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t T = t / P, p = t - T * P;
-    int i, j, k;
-    decode_pos(N, p, i, j, k);
-    if (i < 1 || j < 1 || k < 1 || i + j + k > N - 1) continue;
-    acc += a[T * S + p] * b[T * S + p];
+    const int64_t T = t / ncol;
+    const int c = (int)(t - T * ncol);
+    int d = (int)((sqrt(8.0 * (double)c + 1.0) - 1.0) * 0.5);
+    while ((d + 1) * (d + 2) / 2 <= c) ++d;
+    while (d * (d + 1) / 2 > c) --d;
+    const int j = c - d * (d + 1) / 2, i = d - j;
+    if (i < 1 || j < 1) continue;
+    const double* pa = a + T * S + c;
+    const double* pb = b + T * S + c;
+    for (int k = 1; k <= N - 1 - d; ++k) acc = fma(pa[po_s[k]], pb[po_s[k]], acc);
   }
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n_rows;
        q += (int64_t)gridDim.x * blockDim.x) {

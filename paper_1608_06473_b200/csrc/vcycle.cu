@@ -39,49 +39,80 @@ __device__ __forceinline__ bool owns(uint16_t own, int N, int i, int j, int k) {
   return (own >> (10 + sup[0])) & 1;
 }
 
-// partial restriction at every coarse lattice node of every macro
-__global__ void k_restrict_partial(int Nf, int64_t Sf, int64_t Sc, int64_t Pc, const uint16_t* __restrict__ own,
-                                   const double* __restrict__ rf, double* __restrict__ fc) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t T = blockIdx.y;
-  if (p >= Pc) return;
-  const int Nc = Nf / 2;
-  int i, j, k;
-  decode_pos(Nc, p, i, j, k);
-  const uint16_t om = own[T];
-  const double* r = rf + T * Sf;
-  const int fi = 2 * i, fj = 2 * j, fk = 2 * k;
-  double acc = owns(om, Nf, fi, fj, fk) ? r[lattice_pos(Nf, fi, fj, fk)] : 0.0;
-  double half = 0.0;
-  for (int w = 0; w < 15; ++w) {
-    if (w == kMC) continue;
-    const int a = fi + kDir[w][0], b = fj + kDir[w][1], cc = fk + kDir[w][2];
-    if (a < 0 || b < 0 || cc < 0 || a + b + cc > Nf) continue;
-    if (owns(om, Nf, a, b, cc)) half += r[lattice_pos(Nf, a, b, cc)];
-  }
-  fc[T * Sc + p] = acc + 0.5 * half;
+// Lattice position of (i, j, k) from a shared-memory plane-offset table.
+__device__ __forceinline__ int64_t lpos(const int64_t* po, int i, int j, int k) { return po[k] + col_idx(i, j); }
+
+__device__ __forceinline__ void col_of(int c, int& i, int& j) {
+  int d = (int)((sqrt(8.0 * (double)c + 1.0) - 1.0) * 0.5);
+  while ((d + 1) * (d + 2) / 2 <= c) ++d;
+  while (d * (d + 1) / 2 > c) --d;
+  j = c - d * (d + 1) / 2;
+  i = d - j;
 }
 
-// u_f += P u_c at every fine lattice node of every macro
+// partial restriction at every coarse lattice node of every macro: thread =
+// coarse lattice column (i, j) of macro blockIdx.y, marching k (no per-node
+// position decode; plane offsets from shared memory)
+__global__ void k_restrict_partial(int Nf, int64_t Sf, int64_t Sc, int64_t Pc, const uint16_t* __restrict__ own,
+                                   const double* __restrict__ rf, double* __restrict__ fc) {
+  __shared__ int64_t pof[258], poc[130];
+  const int Nc = Nf / 2;
+  for (int k = threadIdx.x; k <= Nf; k += blockDim.x) pof[k] = plane_off(Nf, k);
+  for (int k = threadIdx.x; k <= Nc; k += blockDim.x) poc[k] = plane_off(Nc, k);
+  __syncthreads();
+  (void)Pc;
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= (Nc + 1) * (Nc + 2) / 2) return;
+  const int64_t T = blockIdx.y;
+  int i, j;
+  col_of(c, i, j);
+  const uint16_t om = own[T];
+  const double* r = rf + T * Sf;
+  double* out = fc + T * Sc + c;
+  const int fi = 2 * i, fj = 2 * j;
+  for (int k = 0; k <= Nc - i - j; ++k) {
+    const int fk = 2 * k;
+    double acc = owns(om, Nf, fi, fj, fk) ? r[lpos(pof, fi, fj, fk)] : 0.0;
+    double half = 0.0;
+    for (int w = 0; w < 15; ++w) {
+      if (w == kMC) continue;
+      const int a = fi + kDir[w][0], b = fj + kDir[w][1], cc = fk + kDir[w][2];
+      if (a < 0 || b < 0 || cc < 0 || a + b + cc > Nf) continue;
+      if (owns(om, Nf, a, b, cc)) half += r[lpos(pof, a, b, cc)];
+    }
+    out[poc[k]] = acc + 0.5 * half;
+  }
+}
+
+// u_f += P u_c at every fine lattice node of every macro: thread = fine lattice
+// column (i, j) of macro blockIdx.y, marching k
 __global__ void k_prolong_add(int Nf, int64_t Sf, int64_t Sc, int64_t Pf, const double* __restrict__ uc,
                               double* __restrict__ uf) {
-  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t T = blockIdx.y;
-  if (p >= Pf) return;
+  __shared__ int64_t pof[258], poc[130];
   const int Nc = Nf / 2;
-  int i, j, k;
-  decode_pos(Nf, p, i, j, k);
-  const double* c = uc + T * Sc;
-  const int par = (i & 1) | ((j & 1) << 1) | ((k & 1) << 2);
-  double v;
-  if (par == 0) {
-    v = c[lattice_pos(Nc, i / 2, j / 2, k / 2)];
-  } else {
-    const int* d = kParityDir[par];
-    v = 0.5 * (c[lattice_pos(Nc, (i - d[0]) / 2, (j - d[1]) / 2, (k - d[2]) / 2)] +
-               c[lattice_pos(Nc, (i + d[0]) / 2, (j + d[1]) / 2, (k + d[2]) / 2)]);
+  for (int k = threadIdx.x; k <= Nf; k += blockDim.x) pof[k] = plane_off(Nf, k);
+  for (int k = threadIdx.x; k <= Nc; k += blockDim.x) poc[k] = plane_off(Nc, k);
+  __syncthreads();
+  (void)Pf;
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= (Nf + 1) * (Nf + 2) / 2) return;
+  const int64_t T = blockIdx.y;
+  int i, j;
+  col_of(col, i, j);
+  const double* cu = uc + T * Sc;
+  double* out = uf + T * Sf + col;
+  for (int k = 0; k <= Nf - i - j; ++k) {
+    const int par = (i & 1) | ((j & 1) << 1) | ((k & 1) << 2);
+    double v;
+    if (par == 0) {
+      v = cu[lpos(poc, i / 2, j / 2, k / 2)];
+    } else {
+      const int* d = kParityDir[par];
+      v = 0.5 * (cu[lpos(poc, (i - d[0]) / 2, (j - d[1]) / 2, (k - d[2]) / 2)] +
+                 cu[lpos(poc, (i + d[0]) / 2, (j + d[1]) / 2, (k + d[2]) / 2)]);
+    }
+    out[pof[k]] += v;
   }
-  uf[T * Sf + p] += v;
 }
 
 // CG vector updates with device scalars s[0] = rr, s[1] = pAp, s[2] = rr_new
@@ -161,7 +192,7 @@ static hhg_status coarse_cg(Ctx* c, int L, int iters, double* x, const double* b
 static hhg_status restrict_to(Ctx* c, int Lf, const double* rf, double* fc) {
   Level& F = c->levels[Lf];
   Level& C = c->levels[Lf - 1];
-  dim3 grid(nblk(C.P, 128), (unsigned)c->nt_local);
+  dim3 grid(nblk((int64_t)(C.N + 1) * (C.N + 2) / 2, 128), (unsigned)c->nt_local);  // coarse columns
   hhg_status st;
   if (c->nt_blocks > c->nt_local)  // ghost blocks hold no partial sums
     HHG_CK(c, cudaMemsetAsync(fc + c->nt_local * C.S, 0, (c->nt_blocks - c->nt_local) * C.S * sizeof(double),
@@ -180,7 +211,7 @@ static hhg_status restrict_to(Ctx* c, int Lf, const double* rf, double* fc) {
 static hhg_status prolong_add(Ctx* c, int Lf, const double* uc, double* uf) {
   Level& F = c->levels[Lf];
   Level& C = c->levels[Lf - 1];
-  dim3 grid(nblk(F.P, 128), (unsigned)c->nt_local);
+  dim3 grid(nblk((int64_t)(F.N + 1) * (F.N + 2) / 2, 128), (unsigned)c->nt_local);  // fine columns
   k_prolong_add<<<grid, 128, 0, c->stream>>>(F.N, F.S, C.S, F.P, uc, uf);
   HHG_LAUNCHED(c);
   return dist_sync(c, F, uf);  // ghost-block slots of the other ranks' macros

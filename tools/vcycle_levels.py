@@ -39,10 +39,10 @@ for Lt in range(3, L + 1):
     lpc = (ctx.kernel_launches - l0) / 2
     ctx.vcycle(Lt, u, f, n_cycles=2)  # unprofiled (HHG_VCYCLE_GRAPH=1: captures the graph)
     e0.record()
-    ctx.vcycle(Lt, u, f, n_cycles=3)  # replays the cached graph
+    ctx.vcycle(Lt, u, f, n_cycles=3)  # unprofiled (replays the cached graph with HHG_VCYCLE_GRAPH=1)
     e1.record()
     torch.cuda.synchronize()
     t3 = e0.elapsed_time(e1) / 3
-    print(f"levels 2..{Lt}: eager {tprof:.2f} ms/cycle (profiled), graph replay {t3:.2f} ms/cycle, "
+    print(f"levels 2..{Lt}: eager {tprof:.2f} ms/cycle (profiled), unprofiled {t3:.2f} ms/cycle, "
           f"launches/cycle {lpc:.0f}  [{parts}]",
           flush=True)
