@@ -248,13 +248,18 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   }
   double* const optr = out + T * S + q.c;
   const double* const fptr = f + T * S + q.c;
-  // residual: f of node k+1 is loaded one step ahead (its latency hides behind a step)
-  double fnext = 0.0;
-  if (MODE == kModeResid && q.active && 1 <= q.len) fnext = __ldg(fptr + po1);
+  // residual: f is loaded FPD steps ahead (its HBM latency hides behind them)
+  constexpr int FPD = 3;
+  double fq[FPD];
+#pragma unroll
+  for (int x = 0; x < FPD; ++x)
+    fq[x] = (MODE == kModeResid && q.active && 1 + x <= q.len) ? __ldg(fptr + sm.po[1 + x]) : 0.0;
   for (int k = 1; k <= b.kmax; ++k) {
     const int po2 = sm.po[k + 1];
-    const double fv = fnext;
-    if (MODE == kModeResid && q.active && k + 1 <= q.len) fnext = __ldg(fptr + po2);
+    const double fv = fq[0];
+#pragma unroll
+    for (int x = 0; x + 1 < FPD; ++x) fq[x] = fq[x + 1];
+    if (MODE == kModeResid) fq[FPD - 1] = (q.active && k + FPD <= q.len) ? __ldg(fptr + sm.po[k + FPD]) : 0.0;
     mbar_wait(&sm.bars[(k + 1) & (kRing - 1)], ((k + 1) / kRing) & 1);
     if (q.active && k <= q.len) {
       const double* Pk = sptr(k, po1);
