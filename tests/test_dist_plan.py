@@ -1,4 +1,5 @@
-"""Multi-rank host logic on CPU (gloo, world size 2 and 3): macro partition,
+"""Multi-rank host logic on CPU (gloo, world size 2, 3, 4 and 8 -- the last two on
+the bench's 4- and 8-GPU weak-scaling meshes, 1920 and 3840 macros): macro partition,
 owner-computes rows, ghost blocks and the exchange plan of libhhg, built in
 plan-only contexts (no CUDA) and checked end to end: every requested node id
 arrives from its owner (hhg_plan_check), and the owned unknowns of all ranks
@@ -49,7 +50,8 @@ def _worker(rank, world, port, mesh_args, L, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mesh_args,L", [(2, (0, 2), 4), (3, (0, 1), 3), (2, (1, 1), 3)])
+@pytest.mark.parametrize("world,mesh_args,L", [(2, (0, 2), 4), (3, (0, 1), 3), (2, (1, 1), 3), (4, (2, 2), 2),
+                                                 (8, (2, 4), 2)])
 def test_partition_plan_consistent(world, mesh_args, L):
     import torch.multiprocessing as mp
     import __graft_entry__ as ge
