@@ -1,4 +1,4 @@
-"""Multi-rank apply / residual / GS through the C-ABI: 2 ranks as 2 processes
+"""Multi-rank apply / residual / GS through the C-ABI: 2 or 4 ranks as processes
 sharing cuda:0, exchanging ghost values through the library's host transport
 (torch.distributed gloo; the NCCL transport moves the same buffers).  The
 assembled result must match the single-process oracle to 1e-12."""
@@ -68,13 +68,12 @@ def _worker(rank, world, port, mesh_args, L, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mesh_args,L", [((0, 2), 3), ((0, 2), 4)])
-def test_two_ranks_match_oracle(mesh_args, L):
+@pytest.mark.parametrize("world,mesh_args,L", [(2, (0, 2), 3), (2, (0, 2), 4), (4, (0, 2), 3)])
+def test_two_ranks_match_oracle(world, mesh_args, L):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    world = 2
     procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_args, L, q)) for r in range(world)]
     for p in procs:
         p.start()
@@ -90,7 +89,7 @@ def test_two_ranks_match_oracle(mesh_args, L):
     u = synth.uniform_pm1(0, g) * num.unknown_mask
     f = synth.uniform_pm1(1, g) * num.unknown_mask
     rel = lambda a, b: np.linalg.norm(a - b) / np.linalg.norm(b)
-    assert res[0]["owned"] + res[1]["owned"] == int(num.unknown_mask.sum())
+    assert sum(res[r]["owned"] for r in range(world)) == int(num.unknown_mask.sum())
     assert rel(res[0]["y"], solvers.apply(Lt, num, u)) < 1e-12
     r_ref = solvers.residual(Lt, num, u, f)
     assert rel(res[0]["r"], r_ref) < 1e-12
