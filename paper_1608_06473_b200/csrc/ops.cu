@@ -15,6 +15,7 @@
 #include "pmarch.cuh"
 #include "pair.cuh"
 #include "gsq.cuh"
+#include "gswave.cuh"
 #include "femmarch.cuh"
 #include "femew.cuh"
 
@@ -516,6 +517,35 @@ static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f)
   return launch_gs_items_nt<OP, kMarchThreads, 24>(c, lv, u, f);
 }
 
+// Experimental single-pass wavefront GS (gswave.cuh, HHG_GS_KERNEL=wave).
+template <int OP>
+static hhg_status launch_gs_wave(Ctx* c, Level& lv, double* u, const double* f) {
+  const size_t smem = (size_t)kWRing * lv.slot_len * 8 + (kWRing + 4) * 8 + 16 * 8 + (size_t)(lv.N + 2) * 4;
+  static std::map<size_t, int> grids;
+  int& grid = grids[smem];
+  if (grid == 0) {
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_wave<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    int dev = 0, sms = 0, per_sm = 0;
+    HHG_CK(c, cudaGetDevice(&dev));
+    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_wave<OP>, kWThreads, smem));
+    grid = sms * per_sm;
+  }
+  const int nb = (int)lv.bands.size();
+  // halo columns per band must fit the synchronisation warp (N <= 130), and
+  // every band of the last handed-out macro must be resident
+  if (lv.N > 130 || grid <= nb) return HHG_ERR_STATE;
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * sizeof(int), c->stream));
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
+  const int64_t items = c->nt_local * nb;
+  ProfScope ps(c, 1);
+  k_gs_wave<OP><<<(unsigned)std::min<int64_t>(grid, items), kWThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter,
+      lv.d_gs_flags);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
 // Whole volume GS sweep as one continuously pipelined persistent launch (gsq.cuh).
 template <int OP>
 static hhg_status launch_gs_quad(Ctx* c, Level& lv, double* u, const double* f) {
@@ -725,7 +755,8 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
   static int mode = -1;  // HHG_GS_KERNEL: passes -> 4 colour launches, quad -> k_gs_quad, default k_gs_items
   if (mode < 0) {
     const char* e = getenv("HHG_GS_KERNEL");
-    mode = (e && std::string(e) == "passes") ? 1 : (e && std::string(e) == "quad") ? 0 : 2;
+    mode = (e && std::string(e) == "passes") ? 1 : (e && std::string(e) == "quad") ? 0
+           : (e && std::string(e) == "wave") ? 3 : 2;
   }
   const bool march_ok = !force_v1() && !lv.bands.empty() &&
                         ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
@@ -733,7 +764,10 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
     hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_quad<HHG_OP_SURROGATE>(c, lv, u, f)
                                            : launch_gs_quad<HHG_OP_CONST_AFFINE>(c, lv, u, f);
     if (st != HHG_OK) return st;
-  } else if (march_ok && mode == 2 &&
+  } else if (march_ok && mode == 3 &&
+             (op == HHG_OP_SURROGATE ? launch_gs_wave<HHG_OP_SURROGATE>(c, lv, u, f)
+                                     : launch_gs_wave<HHG_OP_CONST_AFFINE>(c, lv, u, f)) == HHG_OK) {
+  } else if (march_ok && (mode == 2 || mode == 3) &&
              (op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
                                      : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f)) == HHG_OK) {
   } else {
@@ -939,3 +973,4 @@ extern "C" int hhg_gs_prof_read(unsigned long long* out) {
   return 0;
 }
 #endif
+
