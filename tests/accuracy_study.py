@@ -16,7 +16,10 @@ The paper's macro mesh is unknown: absolute values are context ("parity
 unpinned"), the trends are the result (quadratic FEM convergence; surrogate
 errors follow FEM until a plateau that drops with H and q).
 
-usage: python tools/accuracy_study.py [out.txt]   (a few minutes on one B200)
+usage: python tests/accuracy_study.py [out.txt]   (a few minutes on one B200)
+
+Test infrastructure (it uses the oracle for the lumped right-hand side and
+the node coordinates), kept under tests/ as the oracle rules require.
 """
 import os
 import sys
@@ -111,7 +114,7 @@ def main():
              "# synthetic icosahedral shells (parity unpinned: the paper's macro mesh is unknown).",
              "# FEM: CG on the exact element-wise operator; LSQP/IPOLY: 10 V(3,3) cycles (j = 2).",
              "# '*' = relative deviation from e_FEM above 10 % (the paper's italic entries).",
-             f"# tools/accuracy_study.py, {time.time() - t0:.0f} s"]
+             f"# tests/accuracy_study.py, {time.time() - t0:.0f} s"]
     for nt, rows in tables:
         lines.append(f"\n{nt} macros")
         names = [v[0] for v in VARIANTS]

@@ -1,5 +1,5 @@
 """Discretisation-error trends of PAPER.md Sec. 4.1 / Table hHstudy on the
-60-macro synthetic shell, solved through the C-ABI (tools/accuracy_study.py:
+60-macro synthetic shell, solved through the C-ABI (tests/accuracy_study.py:
 manufactured solution (r - r1)(r - r2) sin(10x) sin(4y) sin(7z), lumped RHS,
 FEM by CG on the exact element-wise operator, surrogates by 10 V(3,3)
 cycles).  Absolute values are unpinned (the paper's macro mesh is unknown);
@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_hHstudy_trends_60_macros():
-    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
     import accuracy_study as A
     variants = [("FEM", 0, None), ("LSQP1", 1, "lsqp"), ("LSQP2", 2, "lsqp"), ("LSQP3", 3, "lsqp"),
                 ("LSQP2-DD", 2, "lsqp-dd")]
