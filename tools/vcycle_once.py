@@ -1,3 +1,4 @@
+"""One V(3,3) cycle on the 480-macro shell at L = 7 (for ncu launch lists of the multigrid kernels)."""
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, paper_1608_06473_b200 as hhg, synth
