@@ -58,6 +58,26 @@ class GS:
                 u[s] = (f[s] - O @ u) / self.diag[s]
         return u
 
+    def sweep_lex(self, u, f, n=1):
+        """The paper's hybrid smoother with a LEXICOGRAPHIC volume ordering
+        (PAPER.md:1317-1330): the lower-primitive class steps as in `sweep`
+        (R13), then the volume nodes of every macro one at a time,
+        west to east, south to north, bottom to top (i fastest, then j, then k
+        -- the order of the volume ids, `interior_ijk`), each from the newest
+        values (eq. iteration-scheme, IEEE division).  Volume nodes of
+        different macros never couple, so the macro order is immaterial."""
+        u = u * mask(self.num)
+        base_v = self.num.base_v
+        lp = [(s, O) for s, O in zip(self.steps, self.offrows) if s[0] < base_v]
+        ip, ix, dv = self.off.indptr, self.off.indices, self.off.data
+        for _ in range(n):
+            for s, O in lp:
+                u[s] = (f[s] - O @ u) / self.diag[s]
+            for g in range(base_v, self.num.n_total):
+                a, b = ip[g], ip[g + 1]
+                u[g] = (f[g] - dv[a:b] @ u[ix[a:b]]) / self.diag[g]
+        return u
+
 
 def prolongation(mesh, num_c: Numbering, num_f: Numbering, masked=True) -> sp.csr_matrix:
     """P: coarse (N/2) -> fine (N), index-space linear interpolation per macro:
@@ -140,24 +160,27 @@ class Hierarchy:
         # the exact operator L computes the residuals
         return self.L[L] if dd else self.Lt[L]
 
-    def vcycle(self, L, u, f, nu1=3, nu2=3, cg_iters=50, dd=False):
+    def vcycle(self, L, u, f, nu1=3, nu2=3, cg_iters=50, dd=False, lex=False):
+        """lex: the paper's lexicographic hybrid smoother (GS.sweep_lex,
+        PAPER.md:1317-1330) instead of the 4-colour one."""
         if L == self.L_coarse:
             m = mask(self.num[L])
             return m * cg(self.A_coarse, m * f, cg_iters)
-        u = self.gs[L].sweep(u, f, nu1)
+        smooth = self.gs[L].sweep_lex if lex else self.gs[L].sweep
+        u = smooth(u, f, nu1)
         r = residual(self._res_op(L, dd), self.num[L], u, f)
         fc = self.P[L].T @ r
-        uc = self.vcycle(L - 1, np.zeros_like(fc), fc, nu1, nu2, cg_iters, dd)
+        uc = self.vcycle(L - 1, np.zeros_like(fc), fc, nu1, nu2, cg_iters, dd, lex)
         u = u + self.P[L] @ uc
-        return self.gs[L].sweep(u, f, nu2)
+        return smooth(u, f, nu2)
 
-    def solve(self, u, f, n_cycles, nu1=3, nu2=3, cg_iters=50, dd=False):
+    def solve(self, u, f, n_cycles, nu1=3, nu2=3, cg_iters=50, dd=False, lex=False):
         """n_cycles V(nu1, nu2) cycles; history = ||f - A u||_2 after each, A
         the residual operator (L~, or L with double discretisation)."""
         L = self.L_max
         A = self._res_op(L, dd)
         hist = [np.linalg.norm(residual(A, self.num[L], u, f))]
         for _ in range(n_cycles):
-            u = self.vcycle(L, u, f, nu1, nu2, cg_iters, dd)
+            u = self.vcycle(L, u, f, nu1, nu2, cg_iters, dd, lex)
             hist.append(np.linalg.norm(residual(A, self.num[L], u, f)))
         return u, np.array(hist)

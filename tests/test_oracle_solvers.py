@@ -181,3 +181,35 @@ def test_double_discretisation_special_cases():
     mk = numc.unknown_mask
     assert abs(hc[-1] - np.linalg.norm(mk * (fc - A @ (mk * uc)))) <= 1e-12 * hc[0]
     assert hc[-1] < 0.5 * hc[0]
+
+
+def test_lexicographic_gs_is_forward_substitution(shell3):
+    """Lexicographic hybrid GS: after the lower-primitive
+    class steps, the volume update equals the textbook forward substitution
+    (D + L)^-1 (f - U u - A_vb u_b) with L / U the strictly lower / upper
+    parts of the volume block in lexicographic order (scipy's triangular
+    solve); the exact solution is a fixed point."""
+    m, num, Lt, Lx = shell3
+    gs = solvers.GS(Lt, num)
+    g = np.arange(num.n_total)
+    u = synth.uniform_pm1(3, g) * num.unknown_mask
+    f = synth.uniform_pm1(4, g) * num.unknown_mask
+    ul = gs.sweep_lex(u.copy(), f, 1)
+    # reference: class steps of the colour sweep, then a triangular solve
+    ub = u * num.unknown_mask
+    for s, O in zip(gs.steps, gs.offrows):
+        if s[0] < num.base_v:
+            ub[s] = (f[s] - O @ ub) / gs.diag[s]
+    vol = np.arange(num.base_v, num.n_total)
+    mk = sp.diags(num.unknown_mask.astype(float))
+    A = (mk @ Lt @ mk).tocsr()
+    Avv = A[vol][:, vol]
+    rhs = f[vol] - A[vol] @ np.where(np.arange(num.n_total) >= num.base_v, 0.0, ub) - sp.triu(Avv, 1) @ ub[vol]
+    uv = spla.spsolve_triangular(sp.tril(Avv, 0).tocsr(), rhs, lower=True)
+    assert np.abs(ul[vol] - uv).max() <= 1e-12 * np.abs(uv).max()
+    assert np.abs(ul[:num.base_v] - ub[:num.base_v]).max() == 0
+    # fixed point: the exact discrete solution is unchanged
+    unk = num.unknown_mask
+    x = np.zeros(num.n_total)
+    x[unk] = spla.spsolve(A[unk][:, unk].tocsc(), f[unk])
+    assert np.abs(gs.sweep_lex(x.copy(), f, 1) - x).max() <= 1e-10 * np.abs(x).max()
