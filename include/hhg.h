@@ -144,6 +144,15 @@ hhg_status hhg_residual(hhg_ctx ctx, int L, hhg_op op, const double* u, const do
  * (HHG_ERR_INVALID). */
 hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n_sweeps);
 
+/* n_sweeps sweeps of the paper's own hybrid smoother with a LEXICOGRAPHIC
+ * volume ordering: the lower-primitive class steps as in
+ * hhg_gs_sweep (R13), then the volume nodes of every macro visited west to
+ * east (i), south to north (j), bottom to top (k), each from the newest values
+ * -- executed exactly as hyperplanes i + 2j + 3k in increasing order (no two
+ * neighbours share one; predecessors lie on lower ones).  Same arguments and
+ * errors as hhg_gs_sweep. */
+hhg_status hhg_gs_sweep_lex(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n_sweeps);
+
 /* n_cycles V(nu1,nu2) cycles from level L down to L_coarse:
  * GS smoothing with `op` on every level, residual, restriction R = P^T, coarse
  * grid solved by coarse_cg_iters CG iterations from zero on the exact FEM
@@ -166,6 +175,13 @@ hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int co
 hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
                          hhg_op smoother_op, hhg_op residual_op, double* u, const double* f, int n_cycles,
                          double* res_hist);
+
+/* The general form of hhg_vcycle / hhg_vcycle_dd: lexicographic != 0 smooths
+ * with hhg_gs_sweep_lex's ordering on every level instead of the 4 colours
+ * (the paper's smoother; compare convergence per cycle). */
+hhg_status hhg_vcycle_ex(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
+                         hhg_op smoother_op, hhg_op residual_op, int lexicographic, double* u, const double* f,
+                         int n_cycles, double* res_hist);
 
 /* Canonical global vector (length n_global_nodes, DESIGN.md numbering:
  * vertices, edges, faces, volumes) <-> local layout.  gather writes every

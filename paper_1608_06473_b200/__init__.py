@@ -47,6 +47,8 @@ def lib():
     L.hhg_gs_sweep.argtypes = [P, I32, I32, P, P, I32]
     L.hhg_vcycle.argtypes = [P, I32, I32, I32, I32, I32, I32, P, P, I32, P]
     L.hhg_vcycle_dd.argtypes = [P, I32, I32, I32, I32, I32, I32, I32, P, P, I32, P]
+    L.hhg_vcycle_ex.argtypes = [P, I32, I32, I32, I32, I32, I32, I32, I32, P, P, I32, P]
+    L.hhg_gs_sweep_lex.argtypes = [P, I32, I32, P, P, I32]
     L.hhg_gather_global.argtypes = [P, I32, P, P]
     L.hhg_scatter_global.argtypes = [P, I32, P, P]
     L.hhg_sync_copies.argtypes = [P, I32, P]
@@ -69,7 +71,8 @@ def lib():
     L.hhg_nccl_unique_id.argtypes = [P]
     L.hhg_nccl_unique_id.restype = ctypes.c_int
     for name in ("hhg_setup_macro_mesh", "hhg_fit_surrogates", "hhg_vector_layout", "hhg_apply",
-                 "hhg_residual", "hhg_gs_sweep", "hhg_vcycle", "hhg_vcycle_dd", "hhg_gather_global",
+                 "hhg_residual", "hhg_gs_sweep", "hhg_gs_sweep_lex", "hhg_vcycle", "hhg_vcycle_dd",
+                 "hhg_vcycle_ex", "hhg_gather_global",
                  "hhg_scatter_global", "hhg_sync_copies", "hhg_eval_stencils"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
@@ -234,17 +237,26 @@ class Ctx:
                                            ctypes.byref(nv) if norm else None))
         return nv.value if norm else None
 
-    def gs_sweep(self, L, u, f, n_sweeps=1, op="surrogate"):
+    def gs_sweep(self, L, u, f, n_sweeps=1, op="surrogate", lexicographic=False):
+        """Multicolour GS sweeps in place (hhg_gs_sweep), or the paper's
+        lexicographic volume ordering (hhg_gs_sweep_lex)."""
         n = self.layout(L)[0]
-        self._check(self._lib.hhg_gs_sweep(self.h, L, OPS[op], _ptr(u, n), _ptr(f, n), n_sweeps))
+        fn = self._lib.hhg_gs_sweep_lex if lexicographic else self._lib.hhg_gs_sweep
+        self._check(fn(self.h, L, OPS[op], _ptr(u, n), _ptr(f, n), n_sweeps))
         return u
 
-    def vcycle(self, L, u, f, n_cycles=1, nu1=3, nu2=3, L_coarse=2, cg_iters=50, op="surrogate", residual_op=None):
+    def vcycle(self, L, u, f, n_cycles=1, nu1=3, nu2=3, L_coarse=2, cg_iters=50, op="surrogate", residual_op=None,
+               lexicographic=False):
         """V(nu1,nu2) cycles in place on u; residual_op (e.g. "fem") selects
-        double discretisation (hhg_vcycle_dd)."""
+        double discretisation (hhg_vcycle_dd), lexicographic the paper's
+        lexicographic smoother (hhg_vcycle_ex)."""
         n = self.layout(L)[0]
         hist = np.zeros(n_cycles + 1)
-        if residual_op is None:
+        if lexicographic:
+            rop = OPS[residual_op if residual_op is not None else op]
+            self._check(self._lib.hhg_vcycle_ex(self.h, L, nu1, nu2, L_coarse, cg_iters, OPS[op], rop, 1,
+                                                _ptr(u, n), _ptr(f, n), n_cycles, hist.ctypes.data))
+        elif residual_op is None:
             self._check(self._lib.hhg_vcycle(self.h, L, nu1, nu2, L_coarse, cg_iters, OPS[op], _ptr(u, n),
                                              _ptr(f, n), n_cycles, hist.ctypes.data))
         else:

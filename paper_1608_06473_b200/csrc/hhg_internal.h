@@ -332,7 +332,7 @@ hhg_status face_sum_copies(Ctx* c, Level& lv, double* v);
 
 // Operator pieces shared by ops.cu and vcycle.cu
 hhg_status apply_dev(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* y);
-hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f);
+hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, bool lex = false);
 hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out);
 hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* d_out);
 hhg_status zero_dir_slots(Ctx* c, Level& lv, double* out);

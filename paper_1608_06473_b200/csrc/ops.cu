@@ -16,6 +16,7 @@
 #include "pair.cuh"
 #include "gsq.cuh"
 #include "gswave.cuh"
+#include "gslex.cuh"
 #include "femmarch.cuh"
 #include "femew.cuh"
 
@@ -732,7 +733,33 @@ hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out) {
   return HHG_OK;
 }
 
-hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
+// lexicographic volume GS (gslex.cuh): one CTA per macro
+static hhg_status launch_gs_lex(Ctx* c, Level& lv, int op, double* u, const double* f) {
+  const size_t smem = lex_smem_bytes(lv.N);
+  static bool attr = false;
+  if (!attr) {
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_lex<HHG_OP_SURROGATE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+    HHG_CK(c, cudaFuncSetAttribute(k_gs_lex<HHG_OP_CONST_AFFINE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kMaxDynSmem));
+    attr = true;
+  }
+  if (lv.N < 4) return HHG_OK;  // no interior nodes
+  if (op == HHG_OP_SURROGATE && !lv.d_coef10) return set_err(c, HHG_ERR_STATE, "gs_lex: surrogate not fitted");
+  ProfScope ps(c, 1);
+  for (int64_t T0 = 0; T0 < c->nt_local; T0 += 65535) {
+    const unsigned nt = (unsigned)std::min<int64_t>(65535, c->nt_local - T0);
+    if (op == HHG_OP_SURROGATE)
+      k_gs_lex<HHG_OP_SURROGATE><<<nt, kLexThreads, smem, c->stream>>>(lv.N, lv.S, lv.d_coef10, lv.d_cons, u, f,
+                                                                       (int)T0);
+    else
+      k_gs_lex<HHG_OP_CONST_AFFINE><<<nt, kLexThreads, smem, c->stream>>>(lv.N, lv.S, lv.d_coef10, lv.d_cons, u,
+                                                                          f, (int)T0);
+    HHG_LAUNCHED(c);
+  }
+  return HHG_OK;
+}
+
+hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, bool lex) {
   const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_val_cons : lv.d_val;
   for (int s = 0; s < kNumLpSteps; ++s) {
     if (s >= kStepFace0) {  // face colours: structured face rows
@@ -751,6 +778,11 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f) {
     // the next class step reads this step's values on every rank
     hhg_status sts = dist_sync(c, lv, u);
     if (sts != HHG_OK) return sts;
+  }
+  if (lex) {  // the paper's lexicographic volume ordering
+    hhg_status st = launch_gs_lex(c, lv, op, u, f);
+    if (st != HHG_OK) return st;
+    return dist_sync(c, lv, u);
   }
   static int mode = -1;  // HHG_GS_KERNEL: passes -> 4 colour launches, quad -> k_gs_quad, default k_gs_items
   if (mode < 0) {
@@ -821,7 +853,7 @@ extern "C" hhg_status hhg_residual(hhg_ctx ctx, int L, hhg_op op, const double* 
   return unstage(c, sr, lv.n_local);
 }
 
-extern "C" hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n) {
+static hhg_status gs_sweep_api(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n, bool lex) {
   Ctx* c = (Ctx*)ctx;
   hhg_status st = check_call(c, L, op, true);
   if (st != HHG_OK) return st;
@@ -831,8 +863,18 @@ extern "C" hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, con
   if ((st = stage(c, 0, u, lv.n_local, true, su)) != HHG_OK) return st;
   if ((st = stage(c, 1, f, lv.n_local, true, sf)) != HHG_OK) return st;
   for (int s = 0; s < n; ++s)
-    if ((st = gs_sweep_dev(c, lv, op, su.dev, sf.dev)) != HHG_OK) return st;
+    if ((st = gs_sweep_dev(c, lv, op, su.dev, sf.dev, lex)) != HHG_OK) return st;
   return unstage(c, su, lv.n_local);
+}
+
+extern "C" hhg_status hhg_gs_sweep(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n) {
+  return gs_sweep_api(ctx, L, op, u, f, n, false);
+}
+
+extern "C" hhg_status hhg_gs_sweep_lex(hhg_ctx ctx, int L, hhg_op op, double* u, const double* f, int n) {
+  Ctx* c = (Ctx*)ctx;
+  if (c && op == HHG_OP_FEM_ELEMENTWISE) return set_err(c, HHG_ERR_INVALID, "FEM is not a smoother");
+  return gs_sweep_api(ctx, L, op, u, f, n, true);
 }
 
 extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local, double* glob) {

@@ -219,24 +219,24 @@ static hhg_status prolong_add(Ctx* c, int Lf, const double* uc, double* uf) {
 
 // op: smoother; rop: residual operator (= op, or the exact FEM operator for
 // double discretisation)
-static hhg_status vcycle_rec(Ctx* c, int L, int Lc, int nu1, int nu2, int cg_iters, int op, int rop, double* u,
-                             const double* f) {
+static hhg_status vcycle_rec(Ctx* c, int L, int Lc, int nu1, int nu2, int cg_iters, int op, int rop, bool lex,
+                             double* u, const double* f) {
   hhg_status st;
   if (L == Lc) return coarse_cg(c, L, cg_iters, u, f);
   Level& lv = c->levels[L];
   for (int s = 0; s < nu1; ++s)
-    if ((st = gs_sweep_dev(c, lv, op, u, f)) != HHG_OK) return st;
+    if ((st = gs_sweep_dev(c, lv, op, u, f, lex)) != HHG_OK) return st;
   if ((st = level_vec(c, c->vc_r, L)) != HHG_OK) return st;
   if ((st = level_vec(c, c->vc_u, L - 1)) != HHG_OK) return st;
   if ((st = level_vec(c, c->vc_f, L - 1)) != HHG_OK) return st;
   if ((st = apply_dev(c, lv, rop, 1 /*residual*/, u, f, c->vc_r[L])) != HHG_OK) return st;
   if ((st = restrict_to(c, L, c->vc_r[L], c->vc_f[L - 1])) != HHG_OK) return st;
   HHG_CK(c, cudaMemsetAsync(c->vc_u[L - 1], 0, c->levels[L - 1].n_local * sizeof(double), c->stream));
-  if ((st = vcycle_rec(c, L - 1, Lc, nu1, nu2, cg_iters, op, rop, c->vc_u[L - 1], c->vc_f[L - 1])) != HHG_OK)
+  if ((st = vcycle_rec(c, L - 1, Lc, nu1, nu2, cg_iters, op, rop, lex, c->vc_u[L - 1], c->vc_f[L - 1])) != HHG_OK)
     return st;
   if ((st = prolong_add(c, L, c->vc_u[L - 1], u)) != HHG_OK) return st;
   for (int s = 0; s < nu2; ++s)
-    if ((st = gs_sweep_dev(c, lv, op, u, f)) != HHG_OK) return st;
+    if ((st = gs_sweep_dev(c, lv, op, u, f, lex)) != HHG_OK) return st;
   return HHG_OK;
 }
 
@@ -245,11 +245,11 @@ static hhg_status vcycle_rec(Ctx* c, int L, int Lc, int nu1, int nu2, int cg_ite
 using namespace hhg;
 
 static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters, hhg_op op,
-                              hhg_op rop, double* u, const double* f, int n_cycles, double* res_hist);
+                              hhg_op rop, bool lex, double* u, const double* f, int n_cycles, double* res_hist);
 
 extern "C" hhg_status hhg_vcycle(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
                                  hhg_op op, double* u, const double* f, int n_cycles, double* res_hist) {
-  return vcycle_impl((Ctx*)ctx, L, nu1, nu2, L_coarse, coarse_cg_iters, op, op, u, f, n_cycles, res_hist);
+  return vcycle_impl((Ctx*)ctx, L, nu1, nu2, L_coarse, coarse_cg_iters, op, op, false, u, f, n_cycles, res_hist);
 }
 
 extern "C" hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
@@ -259,12 +259,23 @@ extern "C" hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_
   if (c && residual_op != HHG_OP_SURROGATE && residual_op != HHG_OP_FEM_ELEMENTWISE &&
       residual_op != HHG_OP_CONST_AFFINE)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle_dd: residual_op");
-  return vcycle_impl(c, L, nu1, nu2, L_coarse, coarse_cg_iters, smoother_op, residual_op, u, f, n_cycles,
+  return vcycle_impl(c, L, nu1, nu2, L_coarse, coarse_cg_iters, smoother_op, residual_op, false, u, f, n_cycles,
                      res_hist);
 }
 
+extern "C" hhg_status hhg_vcycle_ex(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
+                                    hhg_op smoother_op, hhg_op residual_op, int lexicographic, double* u,
+                                    const double* f, int n_cycles, double* res_hist) {
+  Ctx* c = (Ctx*)ctx;
+  if (c && residual_op != HHG_OP_SURROGATE && residual_op != HHG_OP_FEM_ELEMENTWISE &&
+      residual_op != HHG_OP_CONST_AFFINE)
+    return set_err(c, HHG_ERR_INVALID, "hhg_vcycle_ex: residual_op");
+  return vcycle_impl(c, L, nu1, nu2, L_coarse, coarse_cg_iters, smoother_op, residual_op, lexicographic != 0, u,
+                     f, n_cycles, res_hist);
+}
+
 static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters, hhg_op op,
-                              hhg_op rop, double* u, const double* f, int n_cycles, double* res_hist) {
+                              hhg_op rop, bool lex, double* u, const double* f, int n_cycles, double* res_hist) {
   if (!c) return HHG_ERR_INVALID;
   if (c->poisoned) return HHG_ERR_CUDA;
   if (L < 2 || L > c->L_max || L_coarse < 2 || L_coarse > L || nu1 < 0 || nu2 < 0 || coarse_cg_iters < 0 ||
@@ -330,7 +341,8 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
                    !getenv("HHG_GS_KERNEL");
   // the graph is cached on the ctx and reused by later calls with the same
   // signature (levels, smoother, vectors)
-  const std::vector<int64_t> key = {L, L_coarse, nu1, nu2, coarse_cg_iters, (int64_t)op, (int64_t)rop, (int64_t)(intptr_t)du,
+  const std::vector<int64_t> key = {L, L_coarse, nu1, nu2, coarse_cg_iters, (int64_t)op, (int64_t)rop, (int64_t)lex,
+                                    (int64_t)(intptr_t)du,
                                     (int64_t)(intptr_t)df};
   if (c->vc_graph && c->vc_graph_key != key) {
     cudaGraphExecDestroy(c->vc_graph);
@@ -340,7 +352,7 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
   int64_t& graph_launches = c->vc_graph_launches;
   for (int cyc = 0; cyc < n_cycles; ++cyc) {
     if ((cyc == 0 && !gexec) || !use_graph) {
-      if ((st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, rop, du, df)) != HHG_OK) return st;
+      if ((st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, rop, lex, du, df)) != HHG_OK) return st;
     } else {
       if (!gexec) {
         cudaGraph_t graph = nullptr;
@@ -355,7 +367,7 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
           c->stream = orig;
           HHG_CK(c, eb);
         }
-        st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, rop, du, df);
+        st = vcycle_rec(c, L, L_coarse, nu1, nu2, coarse_cg_iters, op, rop, lex, du, df);
         const cudaError_t ee = cudaStreamEndCapture(c->stream, &graph);
         c->stream = orig;
         if (st != HHG_OK) {

@@ -234,3 +234,32 @@ def test_vcycle_double_discretisation_matches_oracle(mesh_name, L, cycles):
     hist = ctx.vcycle(L, du, df, n_cycles=cycles, residual_op="fem")
     assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
     assert rel(ctx.gather_global(L, du), u_ref) < 1e-10
+
+
+@pytest.mark.parametrize("mesh_name,L", [("tet", 3), ("tet", 5), ("shell60", 3), ("shell60", 4), ("shell120", 3)])
+def test_lexicographic_gs_matches_oracle(mesh_name, L):
+    """The paper's lexicographic hybrid smoother run as
+    hyperplane wavefronts on the GPU equals the oracle's node-by-node
+    lexicographic sweep (2 sweeps) to 1e-12."""
+    mesh, num, Lt, A, cf = oracle_case(mesh_name, L)
+    ctx = gpu_ctx(mesh_name, L)
+    u, f = vecs(num)
+    du, df = to_local(ctx, L, u), to_local(ctx, L, f)
+    ctx.gs_sweep(L, du, df, 2, lexicographic=True)
+    u_ref = solvers.GS(Lt, num).sweep_lex(u.copy(), f, 2)
+    assert rel(ctx.gather_global(L, du), u_ref) < TOL
+
+
+@pytest.mark.parametrize("mesh_name,L,cycles", [("tet", 4, 3), ("shell60", 4, 3)])
+def test_vcycle_lexicographic_matches_oracle(mesh_name, L, cycles):
+    """V(3,3) with the lexicographic smoother: residual history and iterate
+    agree with the oracle to 1e-10."""
+    H = oracle_hierarchy(mesh_name, L)
+    num = H.num[L]
+    u0, f = vecs(num, (7, 8))
+    u_ref, hist_ref = H.solve(u0.copy(), f, cycles, lex=True)
+    ctx = gpu_ctx(mesh_name, L)
+    du, df = to_local(ctx, L, u0), to_local(ctx, L, f)
+    hist = ctx.vcycle(L, du, df, n_cycles=cycles, lexicographic=True)
+    assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
+    assert rel(ctx.gather_global(L, du), u_ref) < 1e-10
