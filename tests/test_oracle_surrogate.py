@@ -178,3 +178,34 @@ def test_surrogate_operator_structure():
     assert 0 < asym < 0.05
     Lt2, Lx2, _ = S.surrogate_operator(m, 2, 2)
     assert abs(Lt2 - Lx2).max() == 0.0
+
+
+def test_face_surrogate_special_cases():
+    """Surrogate face rows.  Pins: on an
+    affine macro mesh every face row is constant along the face, so the fit
+    reproduces the exact rows (PAPER.md:638-641 analogue); fitted rows keep
+    zero row sums (the fit is linear and the exact rows sum to zero,
+    PAPER.md:696-717 analogue); on the curved shell the surrogate faces change
+    the operator by a small relative amount that shrinks with H (more macros)."""
+    import numpy as np
+    import synth
+    from oracle import geometry as G, surrogate as S
+    m = synth.shell_mesh(0.55, 1.0, 0, 1)
+    flat = synth.MacroMesh(m.vertices, None, m.tets, m.dirichlet)
+    L = 4
+    num = G.Numbering(flat, 2 ** L)
+    Lt, A, cf = S.surrogate_operator(flat, L, 2, num=num)
+    Lf, _, _ = S.surrogate_operator_faces(flat, L, 2, num=num, A_exact=A, coeffs=cf)
+    unk = np.nonzero(num.unknown_mask)[0]  # Dirichlet rows are not part of the operator
+    assert abs((Lf - Lt)[unk]).max() <= 1e-13 * abs(Lt).max()
+    rel = []
+    for t in (0, 1):  # 60 -> 240 macros: the faces shrink tangentially
+        mc = synth.shell_mesh(0.55, 1.0, t, 1)
+        numc = G.Numbering(mc, 2 ** L)
+        Ltc, Ac, cfc = S.surrogate_operator(mc, L, 2, num=numc)
+        Lfc, _, _ = S.surrogate_operator_faces(mc, L, 2, num=numc, A_exact=Ac, coeffs=cfc)
+        rows = np.nonzero(numc.unknown_mask[numc.base_f:numc.base_v])[0] + numc.base_f
+        rs = np.asarray(Lfc[rows].sum(axis=1)).ravel()
+        assert np.abs(rs).max() <= 1e-13 * abs(Lfc).max()
+        rel.append(abs(Lfc[rows] - Ltc[rows]).max() / abs(Ltc[rows]).max())
+    assert 0 < rel[1] < rel[0] < 0.1, rel
