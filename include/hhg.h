@@ -86,9 +86,16 @@ typedef enum {
   HHG_OP_FEM_ELEMENTWISE = 1, /* exact L: element-wise on-the-fly assembly over
                                  all fine tets, blended geometry (PAPER.md:
                                  1102-1122); comparison path */
-  HHG_OP_CONST_AFFINE = 2     /* CONS: FEM of the unblended (affine) mesh, one
+  HHG_OP_CONST_AFFINE = 2,    /* CONS: FEM of the unblended (affine) mesh, one
                                  constant stencil per macro for volume rows
                                  (PAPER.md:380-384, 886-889); comparison path */
+  HHG_OP_SURROGATE_FACES = 3  /* L~ with the face-node rows from surrogates too
+                                 (PAPER.md:341-345 remark): per
+                                 face and neighbour entry a degree-q polynomial
+                                 in the face coordinates (s, t), least squares
+                                 on the face nodes of the embedded 2^(m+2)
+                                 lattice; edge / vertex rows exact.  Fitted by
+                                 hhg_fit_surrogates; exact at L = 2 */
 } hhg_op;
 
 typedef enum { HHG_FIT_LSQP = 0, HHG_FIT_IPOLY = 1 } hhg_fit_method;

@@ -15,7 +15,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhhg.so")
 
-OPS = {"surrogate": 0, "fem": 1, "fem_elementwise": 1, "const": 2, "const_affine": 2}
+OPS = {"surrogate": 0, "fem": 1, "fem_elementwise": 1, "const": 2, "const_affine": 2, "surrogate_faces": 3}
 FIT = {"lsqp": 0, "ipoly": 1}
 STATUS = {0: "HHG_OK", 1: "HHG_ERR_INVALID", 2: "HHG_ERR_MESH", 3: "HHG_ERR_FIT",
           4: "HHG_ERR_NUMERIC", 5: "HHG_ERR_DIVERGED", 6: "HHG_ERR_CUDA", 7: "HHG_ERR_NCCL",

@@ -96,11 +96,30 @@ __device__ __forceinline__ void load_po(int* po_s, const int* po, int N) {
   __syncthreads();
 }
 
+// Surrogate face weight: degree-q polynomial in index units,
+// exponents (a, b) by degree, b ascending (fit.cu::fit_faces).
+__device__ __forceinline__ double face_poly(const double* __restrict__ cf, int q, int s, int t) {
+  const double ds = (double)s, dt = (double)t;
+  if (q == 2)  // (0,0) (1,0) (0,1) (2,0) (1,1) (0,2)
+    return fma(ds, fma(ds, cf[3], fma(dt, cf[4], cf[1])), fma(dt, fma(dt, cf[5], cf[2]), cf[0]));
+  if (q == 1) return fma(ds, cf[1], fma(dt, cf[2], cf[0]));
+  if (q == 0) return cf[0];
+  double sp[5], tp[5];
+  sp[0] = tp[0] = 1.0;
+  for (int k = 1; k <= q; ++k) sp[k] = sp[k - 1] * s, tp[k] = tp[k - 1] * t;
+  double v = 0.0;
+  int x = 0;
+  for (int d = 0; d <= q; ++d)
+    for (int b = 0; b <= d; ++b) v = fma(cf[x++], sp[d - b] * tp[b], v);
+  return v;
+}
+
 // mode: kModeApply / kModeResid (vol_kernels.cuh values 0 / 1)
 __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
                              const uint32_t* __restrict__ fst, const int* __restrict__ po,
                              const double* __restrict__ val, const double* __restrict__ u,
-                             const double* __restrict__ f, double* __restrict__ out, int mode) {
+                             const double* __restrict__ f, double* __restrict__ out, int mode,
+                             const double* __restrict__ fcoef, int fq) {
   __shared__ int po_s[260];
   load_po(po_s, po, N);
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -110,10 +129,17 @@ __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, con
   const uint32_t st = fst[F.z * nfi + (r - fc * nfi)];
   FaceRowSlots o;
   face_row_slots(F, N, S, po_s, st & 0xffff, st >> 16, o);
-  double acc = val[r] * u[o.cA];
+  const int nfc = (fq + 1) * (fq + 2) / 2;
+  auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
+    return fcoef ? face_poly(fcoef + (fc * 15 + e) * nfc, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
+  };
+  // all neighbour values first (memory-level parallelism), then the weights
+  double un[14];
 #pragma unroll
-  for (int e = 0; e < 14; ++e)
-    if (o.nb[e] >= 0) acc = fma(val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
+  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
+  double acc = wgt(0) * u[o.cA];
+#pragma unroll
+  for (int e = 0; e < 14; ++e) acc = fma(wgt(e + 1), un[e], acc);
   const double res = mode == 1 ? f[o.cA] - acc : acc;
   out[o.cA] = res;
   if (o.cB >= 0) out[o.cB] = res;
@@ -132,7 +158,8 @@ __device__ __forceinline__ bool face_inner(int N, int s, int t) { return s >= 2 
 __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, const FaceLP* __restrict__ flp,
                           const uint32_t* __restrict__ fst, const int* __restrict__ po, int64_t n_frows,
                           const double* __restrict__ val, double* __restrict__ u,
-                          const double* __restrict__ f, double* __restrict__ tmp) {
+                          const double* __restrict__ f, double* __restrict__ tmp,
+                          const double* __restrict__ fcoef, int fq) {
   __shared__ int po_s[260];
   load_po(po_s, po, N);
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -145,11 +172,17 @@ __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, co
   const uint32_t st = fst[F.z * nfi + q];
   FaceRowSlots o;
   face_row_slots(F, N, S, po_s, st & 0xffff, st >> 16, o);
+  const int ncf = (fq + 1) * (fq + 2) / 2;
+  auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
+    return fcoef ? face_poly(fcoef + (fc * 15 + e) * ncf, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
+  };
+  double un[14];
+#pragma unroll
+  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
   double acc = f[o.cA];
 #pragma unroll
-  for (int e = 0; e < 14; ++e)
-    if (o.nb[e] >= 0) acc = fma(-val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
-  const double v = acc / val[r];
+  for (int e = 0; e < 14; ++e) acc = fma(-wgt(e + 1), un[e], acc);
+  const double v = acc / wgt(0);
   if (face_inner(N, st & 0xffff, st >> 16)) {
     u[o.cA] = v;
     if (o.cB >= 0) u[o.cB] = v;
@@ -242,9 +275,10 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 hhg_status face_apply(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* out) {
   if (lv.n_frows == 0) return HHG_OK;
   const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_fval_cons : lv.d_fval;
+  const double* fcoef = op == HHG_OP_SURROGATE_FACES ? lv.d_fcoef : nullptr;
   ProfScope ps(c, 2);
   k_face_apply<<<nblk(lv.n_frows, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, lv.n_frows, lv.d_flp,
-                                                             lv.d_fst, lv.d_po, val, u, f, out, mode);
+                                                             lv.d_fst, lv.d_po, val, u, f, out, mode, fcoef, lv.q);
   HHG_LAUNCHED(c);
   return HHG_OK;
 }
@@ -253,10 +287,11 @@ hhg_status face_gs_step(Ctx* c, Level& lv, int op, int colour, double* u, const 
   const int64_t nfc = lv.fcol[colour + 1] - lv.fcol[colour];
   if (lv.n_frows == 0 || nfc == 0) return HHG_OK;
   const double* val = op == HHG_OP_CONST_AFFINE ? lv.d_fval_cons : lv.d_fval;
+  const double* fcoef = op == HHG_OP_SURROGATE_FACES ? lv.d_fcoef : nullptr;
   const int64_t n = nfc * lv.n_flp;
   ProfScope ps(c, 2);
   k_face_gs<<<nblk(n, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, nfc, lv.fcol[colour], lv.d_flp, lv.d_fst,
-                                                 lv.d_po, lv.n_frows, val, u, f, lv.d_ftmp);
+                                                 lv.d_po, lv.n_frows, val, u, f, lv.d_ftmp, fcoef, lv.q);
   HHG_LAUNCHED(c);
   k_face_write<<<nblk(n, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, nfc, lv.fcol[colour], lv.d_flp,
                                                     lv.d_fst, lv.d_po, lv.n_flp, lv.d_ftmp, u);

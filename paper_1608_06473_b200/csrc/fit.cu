@@ -8,6 +8,7 @@
 // once per level on the host by Householder QR and applied to all macros and
 // all 15 right-hand sides as one batched product on the GPU.
 #include <cmath>
+#include <map>
 
 #include "fem_device.cuh"
 #include "hhg_internal.h"
@@ -91,6 +92,73 @@ __global__ void k_fit_coef(const double* __restrict__ pinv, const double* __rest
   const double* b = B + T * ns * 15;
   for (int64_t s = 0; s < ns; ++s) acc += pinv[c * ns + s] * b[s * 15 + w];
   coef[(T * 15 + w) * mq + c] = acc * scale[c];
+}
+
+// Surrogate face polynomials: per face fc and entry e,
+// coef = pinv * (exact weights at the face sample nodes), index units.
+__global__ void k_face_fit(const double* __restrict__ pinv, int ns, int nfc, const double* __restrict__ scale,
+                           const FaceLP* __restrict__ flp, const int* __restrict__ sq, int64_t nfi,
+                           int64_t n_frows, const double* __restrict__ fval, double* __restrict__ fcoef) {
+  const int64_t fc = blockIdx.x;
+  const int t = threadIdx.x;
+  if (t >= 15 * nfc) return;
+  const int e = t / nfc, cc = t % nfc;
+  const int* q = sq + flp[fc].z * ns;
+  const double* v = fval + e * n_frows + fc * nfi;
+  double acc = 0.0;
+  for (int x = 0; x < ns; ++x) acc += pinv[cc * ns + x] * v[q[x]];
+  fcoef[(fc * 15 + e) * nfc + cc] = acc * scale[cc];
+}
+
+static hhg_status fit_faces(Ctx* c, Level& lv, int L, int q, int sampling_j) {
+  if (lv.d_fcoef) cudaFree(lv.d_fcoef);
+  lv.d_fcoef = nullptr;
+  if (lv.n_flp == 0 || L < 3) return HHG_OK;
+  const int N = lv.N;
+  const int nfc = (q + 1) * (q + 2) / 2;
+  std::vector<int> ea, eb;  // face exponents (a, b): by degree, b ascending
+  for (int d = 0; d <= q; ++d)
+    for (int b = 0; b <= d; ++b) ea.push_back(d - b), eb.push_back(b);
+  const int l = L - 2, m = std::min(l, std::max(1, sampling_j));
+  const int Nm = 1 << (m + 2), sc = 1 << (l - m);
+  std::vector<int> st;
+  for (int t = 1; t < Nm - 1; ++t)
+    for (int s = 1; s < Nm - t; ++s) st.push_back(s * sc), st.push_back(t * sc);
+  const int ns = (int)st.size() / 2;
+  if (ns < nfc) return set_err(c, HHG_ERR_FIT, "fewer face samples than coefficients");
+  std::vector<double> A((size_t)ns * nfc);
+  for (int x = 0; x < ns; ++x)
+    for (int cc = 0; cc < nfc; ++cc)
+      A[(size_t)x * nfc + cc] = std::pow((double)st[2 * x] / N, ea[cc]) * std::pow((double)st[2 * x + 1] / N, eb[cc]);
+  std::vector<double> pinv;
+  if (!pinv_qr(A, ns, nfc, pinv)) return set_err(c, HHG_ERR_FIT, "rank-deficient face sampling matrix");
+  std::vector<double> scale(nfc);
+  for (int cc = 0; cc < nfc; ++cc) scale[cc] = std::ldexp(1.0, -L * (ea[cc] + eb[cc]));
+  // row index (within a face) of every sample node, per row mode z
+  const int64_t nfi = lv.gi.nfi;
+  std::vector<int> sq(3 * (size_t)ns);
+  for (int z = 0; z < 3; ++z) {
+    std::map<uint32_t, int> inv;
+    for (int64_t x = 0; x < nfi; ++x) inv[lv.h_fst[z * nfi + x]] = (int)x;
+    for (int x = 0; x < ns; ++x) sq[z * ns + x] = inv.at((uint32_t)st[2 * x] | ((uint32_t)st[2 * x + 1] << 16));
+  }
+  double *d_pinv, *d_scale;
+  int* d_sq;
+  HHG_CK(c, cudaMalloc(&d_pinv, pinv.size() * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&d_scale, nfc * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&d_sq, sq.size() * sizeof(int)));
+  HHG_CK(c, cudaMalloc(&lv.d_fcoef, (size_t)lv.n_flp * 15 * nfc * sizeof(double)));
+  HHG_CK(c, cudaMemcpy(d_pinv, pinv.data(), pinv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  HHG_CK(c, cudaMemcpy(d_scale, scale.data(), nfc * sizeof(double), cudaMemcpyHostToDevice));
+  HHG_CK(c, cudaMemcpy(d_sq, sq.data(), sq.size() * sizeof(int), cudaMemcpyHostToDevice));
+  k_face_fit<<<(unsigned)lv.n_flp, ((15 * nfc + 31) / 32) * 32, 0, c->stream>>>(
+      d_pinv, ns, nfc, d_scale, lv.d_flp, d_sq, nfi, lv.n_frows, lv.d_fval, lv.d_fcoef);
+  HHG_LAUNCHED(c);
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_pinv);
+  cudaFree(d_scale);
+  cudaFree(d_sq);
+  return HHG_OK;
 }
 
 // Level 2 (l = 0): single interior node, exact stencil as the constant term.
@@ -213,6 +281,7 @@ extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method meth
     cudaFree(d_scale);
     hhg_status st2 = make10(lv);
     if (st2 != HHG_OK) return st2;
+    if ((st2 = fit_faces(c, lv, L, q, sampling_j)) != HHG_OK) return st2;
     lv.fitted = true;
   }
   HHG_CK(c, cudaStreamSynchronize(c->stream));

@@ -16,6 +16,8 @@ namespace hhg {
 // Stencil directions (reading R7); opposite(w) = 14 - w.
 // ---------------------------------------------------------------------------
 constexpr int kMC = 7;
+// L~ with surrogate face rows too; the public enum value
+// HHG_OP_SURROGATE_FACES lives in include/hhg.h
 #define HHG_DIRS_INIT                                                                     \
   {{0, 0, -1}, {1, 0, -1}, {0, 1, -1}, {-1, 1, -1}, {0, -1, 0}, {1, -1, 0}, {-1, 0, 0}, \
    {0, 0, 0},  {1, 0, 0},  {-1, 1, 0}, {0, 1, 0},   {1, -1, 1}, {0, -1, 1}, {-1, 0, 1}, \
@@ -177,6 +179,7 @@ struct Level {
   uint32_t* d_fst = nullptr;       // [3][nfi] s | t << 16 for q, per row mode z
   int* d_fcidx = nullptr;          // [3][nfi] canonical in-face index of q
   double* d_fval = nullptr;        // [15][n_frows] exact FEM, blended
+  double* d_fcoef = nullptr;       // [n_flp][15][(q+1)(q+2)/2] surrogate face polynomials
   double* d_fval_cons = nullptr;   // [15][n_frows] exact FEM, affine
   double* d_ftmp = nullptr;        // [n_frows] GS scratch
   int* d_po = nullptr;             // [N+2] plane offsets

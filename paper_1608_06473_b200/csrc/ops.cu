@@ -238,8 +238,8 @@ static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
   if (c->poisoned) return HHG_ERR_CUDA;
   if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context (hhg_set_host_transport host_only)");
   if (L < 2 || L > c->L_max) return set_err(c, HHG_ERR_INVALID, "L out of range");
-  if (op < 0 || op > 2) return set_err(c, HHG_ERR_INVALID, "bad op");
-  if (op == HHG_OP_SURROGATE && !c->levels[L].fitted)
+  if (op < 0 || op > 3) return set_err(c, HHG_ERR_INVALID, "bad op");
+  if ((op == HHG_OP_SURROGATE || op == HHG_OP_SURROGATE_FACES) && !c->levels[L].fitted)
     return set_err(c, HHG_ERR_STATE, "hhg_fit_surrogates must be called before using the surrogate operator");
   (void)smoother;
   return HHG_OK;
@@ -580,6 +580,7 @@ static hhg_status launch_gs_quad(Ctx* c, Level& lv, double* u, const double* f) 
 
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
                               const double* f, double* out) {
+  if (op == HHG_OP_SURROGATE_FACES) op = HHG_OP_SURROGATE;  // volume rows: the surrogate
   if (mode == kModeGS && !force_v1() && !lv.bands.empty()) {
     if (op == HHG_OP_SURROGATE && lv.d_coef10) return launch_gs_march<HHG_OP_SURROGATE>(c, lv, colour, out, f);
     if (op == HHG_OP_CONST_AFFINE) return launch_gs_march<HHG_OP_CONST_AFFINE>(c, lv, colour, out, f);
@@ -779,6 +780,7 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
     hhg_status sts = dist_sync(c, lv, u);
     if (sts != HHG_OK) return sts;
   }
+  if (op == HHG_OP_SURROGATE_FACES) op = HHG_OP_SURROGATE;  // volume rows: the surrogate
   if (lex) {  // the paper's lexicographic volume ordering
     hhg_status st = launch_gs_lex(c, lv, op, u, f);
     if (st != HHG_OK) return st;

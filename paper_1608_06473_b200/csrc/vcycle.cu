@@ -257,7 +257,7 @@ extern "C" hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_
                                     int n_cycles, double* res_hist) {
   Ctx* c = (Ctx*)ctx;
   if (c && residual_op != HHG_OP_SURROGATE && residual_op != HHG_OP_FEM_ELEMENTWISE &&
-      residual_op != HHG_OP_CONST_AFFINE)
+      residual_op != HHG_OP_CONST_AFFINE && residual_op != HHG_OP_SURROGATE_FACES)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle_dd: residual_op");
   return vcycle_impl(c, L, nu1, nu2, L_coarse, coarse_cg_iters, smoother_op, residual_op, false, u, f, n_cycles,
                      res_hist);
@@ -268,7 +268,7 @@ extern "C" hhg_status hhg_vcycle_ex(hhg_ctx ctx, int L, int nu1, int nu2, int L_
                                     const double* f, int n_cycles, double* res_hist) {
   Ctx* c = (Ctx*)ctx;
   if (c && residual_op != HHG_OP_SURROGATE && residual_op != HHG_OP_FEM_ELEMENTWISE &&
-      residual_op != HHG_OP_CONST_AFFINE)
+      residual_op != HHG_OP_CONST_AFFINE && residual_op != HHG_OP_SURROGATE_FACES)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle_ex: residual_op");
   return vcycle_impl(c, L, nu1, nu2, L_coarse, coarse_cg_iters, smoother_op, residual_op, lexicographic != 0, u,
                      f, n_cycles, res_hist);
@@ -281,8 +281,8 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
   if (L < 2 || L > c->L_max || L_coarse < 2 || L_coarse > L || nu1 < 0 || nu2 < 0 || coarse_cg_iters < 0 ||
       n_cycles < 0 || !u || !f || (const double*)u == f)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: bad arguments");
-  if (op != HHG_OP_SURROGATE && op != HHG_OP_CONST_AFFINE)
-    return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: smoother op must be SURROGATE or CONST_AFFINE");
+  if (op != HHG_OP_SURROGATE && op != HHG_OP_CONST_AFFINE && op != HHG_OP_SURROGATE_FACES)
+    return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: smoother op must be SURROGATE(_FACES) or CONST_AFFINE");
   if (c->host_only)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: needs device vectors (host_only context)");
   for (int l = L_coarse; l <= L; ++l)

@@ -11,6 +11,7 @@ lumped-mass discrete L2 norm sqrt(sum_I m_I e_I^2) over the unknowns.
               V-cycle whose coarsest level is the finest (hhg_vcycle L_coarse = L).
   LSQP/IPOLY: 10 V(3,3) cycles with the surrogate operator.
   LSQP2-DD:   10 V(3,3) cycles, surrogate smoother, exact residual.
+  LSQP2-F:    10 V(3,3) cycles with surrogate face rows as well.
 
 The paper's macro mesh is unknown: absolute values are context ("parity
 unpinned"), the trends are the result (quadratic FEM convergence; surrogate
@@ -88,6 +89,9 @@ def solve_error(ctx, L, du, df, name, q, method, cg_iters, cycles, unk, ue, mass
         # CG on the exact operator: a "V-cycle" whose coarsest level is L itself
         # (level 2: every row is exact, l = 0)
         ctx.vcycle(L, du, df, n_cycles=1, L_coarse=L, cg_iters=cg_iters)
+    elif method == "lsqp-faces":  # surrogate face rows too
+        ctx.fit(q, "lsqp", 2)
+        ctx.vcycle(L, du, df, n_cycles=cycles, op="surrogate_faces")
     elif method == "lsqp-dd":  # double discretisation: exact residual
         ctx.fit(q, "lsqp", 2)
         ctx.vcycle(L, du, df, n_cycles=cycles, residual_op="fem")
@@ -102,7 +106,7 @@ def solve_error(ctx, L, du, df, name, q, method, cg_iters, cycles, unk, ue, mass
 
 # IPOLY: the paper gives interpolation points for q = 2 only
 VARIANTS = [("FEM", 0, None), ("LSQP1", 1, "lsqp"), ("LSQP2", 2, "lsqp"), ("LSQP3", 3, "lsqp"),
-            ("IPOLY2", 2, "ipoly"), ("LSQP2-DD", 2, "lsqp-dd")]
+            ("IPOLY2", 2, "ipoly"), ("LSQP2-DD", 2, "lsqp-dd"), ("LSQP2-F", 2, "lsqp-faces")]
 
 
 def main():

@@ -263,3 +263,28 @@ def test_vcycle_lexicographic_matches_oracle(mesh_name, L, cycles):
     hist = ctx.vcycle(L, du, df, n_cycles=cycles, lexicographic=True)
     assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
     assert rel(ctx.gather_global(L, du), u_ref) < 1e-10
+
+
+@functools.lru_cache(maxsize=None)
+def oracle_faces_case(mesh_name, L):
+    mesh, num, Lt, A, cf = oracle_case(mesh_name, L)
+    Lf, _, _ = S.surrogate_operator_faces(mesh, L, 2, num=num, A_exact=A, coeffs=cf)
+    return mesh, num, Lf
+
+
+@pytest.mark.parametrize("mesh_name,L", [("shell60", 3), ("shell60", 4), ("shell120", 3), ("shell120", 4)])
+def test_surrogate_faces_operator_matches_oracle(mesh_name, L):
+    """Surrogate face rows: apply, residual and a GS sweep with
+    op = surrogate_faces equal the oracle's operator with fitted face rows
+    (oracle.surrogate.surrogate_operator_faces) to 1e-12."""
+    mesh, num, Lf = oracle_faces_case(mesh_name, L)
+    ctx = gpu_ctx(mesh_name, L)
+    u, f = vecs(num)
+    du, df, dy, dr = to_local(ctx, L, u), to_local(ctx, L, f), ctx.zeros(L), ctx.zeros(L)
+    ctx.apply(L, du, dy, op="surrogate_faces")
+    assert rel(ctx.gather_global(L, dy), solvers.apply(Lf, num, u)) < TOL
+    ctx.residual(L, du, df, dr, op="surrogate_faces")
+    assert rel(ctx.gather_global(L, dr), solvers.residual(Lf, num, u, f)) < TOL
+    ug = du.clone()
+    ctx.gs_sweep(L, ug, df, 1, op="surrogate_faces")
+    assert rel(ctx.gather_global(L, ug), solvers.GS(Lf, num).sweep(u.copy(), f, 1)) < TOL
