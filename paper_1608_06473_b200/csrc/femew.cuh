@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
       double G[3];
 #pragma unroll
       for (int d = 0; d < 3; ++d) G[d] = fma(c1[d], du1, fma(c2[d], du2, c3[d] * du3));
-      const double s = 1.0 / (6.0 * fabs(det));
+      const double s = rcp_nr(6.0 * fabs(det));  // ~1 ulp (R16)
       const double y1 = fma(c1[0], G[0], fma(c1[1], G[1], c1[2] * G[2])) * s;
       const double y2 = fma(c2[0], G[0], fma(c2[1], G[1], c2[2] * G[2])) * s;
       const double y3 = fma(c3[0], G[0], fma(c3[1], G[1], c3[2] * G[2])) * s;
