@@ -133,13 +133,20 @@ __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, con
   auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
     return fcoef ? face_poly(fcoef + (fc * 15 + e) * nfc, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
   };
-  // all neighbour values first (memory-level parallelism), then the weights
-  double un[14];
+  double acc;
+  if (fcoef) {  // all neighbour values first (memory-level parallelism), then the weights
+    double un[14];
 #pragma unroll
-  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
-  double acc = wgt(0) * u[o.cA];
+    for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
+    acc = wgt(0) * u[o.cA];
 #pragma unroll
-  for (int e = 0; e < 14; ++e) acc = fma(wgt(e + 1), un[e], acc);
+    for (int e = 0; e < 14; ++e) acc = fma(wgt(e + 1), un[e], acc);
+  } else {
+    acc = val[r] * u[o.cA];
+#pragma unroll
+    for (int e = 0; e < 14; ++e)
+      if (o.nb[e] >= 0) acc = fma(val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
+  }
   const double res = mode == 1 ? f[o.cA] - acc : acc;
   out[o.cA] = res;
   if (o.cB >= 0) out[o.cB] = res;
@@ -176,13 +183,21 @@ __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, co
   auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
     return fcoef ? face_poly(fcoef + (fc * 15 + e) * ncf, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
   };
-  double un[14];
-#pragma unroll
-  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
   double acc = f[o.cA];
+  double v;
+  if (fcoef) {  // all neighbour values first (memory-level parallelism), then the weights
+    double un[14];
 #pragma unroll
-  for (int e = 0; e < 14; ++e) acc = fma(-wgt(e + 1), un[e], acc);
-  const double v = acc / wgt(0);
+    for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
+#pragma unroll
+    for (int e = 0; e < 14; ++e) acc = fma(-wgt(e + 1), un[e], acc);
+    v = acc / wgt(0);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 14; ++e)
+      if (o.nb[e] >= 0) acc = fma(-val[(e + 1) * n_frows + r], u[o.nb[e]], acc);
+    v = acc / val[r];
+  }
   if (face_inner(N, st & 0xffff, st >> 16)) {
     u[o.cA] = v;
     if (o.cB >= 0) u[o.cB] = v;
