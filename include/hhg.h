@@ -135,8 +135,10 @@ hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method method, int sam
 hhg_status hhg_vector_layout(hhg_ctx ctx, int L, int64_t* n_local_doubles,
                              int64_t* n_owned_unknowns, int64_t* n_global_nodes);
 
-/* y = A u over the unknowns (A = L~, L or CONS by op); y = 0 at Dirichlet
- * slots; all copies of y written.  u and y must not alias. */
+/* y = A u over the unknowns (A = L~, L or CONS by op; PAPER.md:618-636
+ * eq. ts, per-node stencils evaluated on the fly PAPER.md:654-690); y = 0 at
+ * Dirichlet slots; all copies of y written.  u and y must not alias
+ * (HHG_ERR_INVALID); L~ before hhg_fit_surrogates: HHG_ERR_STATE. */
 hhg_status hhg_apply(hhg_ctx ctx, int L, hhg_op op, const double* u, double* y);
 
 /* r = f - A u.  If norm2 != NULL the Euclidean norm of r
@@ -183,9 +185,10 @@ hhg_status hhg_vcycle_dd(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int
                          hhg_op smoother_op, hhg_op residual_op, double* u, const double* f, int n_cycles,
                          double* res_hist);
 
-/* The general form of hhg_vcycle / hhg_vcycle_dd: lexicographic != 0 smooths
- * with hhg_gs_sweep_lex's ordering on every level instead of the 4 colours
- * (the paper's smoother; compare convergence per cycle). */
+/* The general form of hhg_vcycle / hhg_vcycle_dd:
+ * lexicographic != 0 smooths with hhg_gs_sweep_lex's ordering on every level
+ * instead of the 4 colours (the paper's smoother; compare
+ * convergence per cycle).  Arguments and errors as hhg_vcycle_dd. */
 hhg_status hhg_vcycle_ex(hhg_ctx ctx, int L, int nu1, int nu2, int L_coarse, int coarse_cg_iters,
                          hhg_op smoother_op, hhg_op residual_op, int lexicographic, double* u, const double* f,
                          int n_cycles, double* res_hist);
@@ -247,7 +250,10 @@ int64_t hhg_kernel_launches(hhg_ctx ctx);
 hhg_status hhg_profile(hhg_ctx ctx, int enable);
 hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, int64_t* launches);
 
+/* Text of the last error of ctx (owned by ctx, valid until the next call). */
 const char* hhg_last_error(hhg_ctx ctx);
+/* Frees everything ctx owns (device buffers, NCCL communicator, streams,
+ * cached graphs); NULL is a no-op. */
 void hhg_destroy(hhg_ctx ctx);
 
 #ifdef __cplusplus
