@@ -433,16 +433,6 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
   // resident at once (an item waits on its neighbour bands): otherwise use the
   // colour-pass kernels (no cross-CTA waits)
   if (grid <= nb) return HHG_ERR_STATE;
-  // macro group: u and f of G macros (~90 MB) stay L2-resident across the 4
-  // colours, and a colour stage (G x bands items) is several CTA waves long so
-  // that stage c+1 rarely waits for stage c.
-  const double per_macro = 2.0 * (double)lv.S * sizeof(double);
-  static double l2_target = -1.0;
-  if (l2_target < 0) {
-    const char* e = getenv("HHG_GS_GROUP_MB");
-    l2_target = e ? atof(e) * 1e6 : 90.0e6;
-  }
-  int G = (int)std::max(1.0, std::min((double)c->nt_local, l2_target / per_macro));
   static int gated = -1;  // HHG_GS_DEPS=gate -> plane-level progress gating (k_gs_items_p; measured slower)
   if (gated < 0) {
     const char* e = getenv("HHG_GS_DEPS");
@@ -474,7 +464,6 @@ static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double*
       const char* e = getenv("HHG_GS_SCHED");
       dyn = (e && std::string(e) == "static") ? 0 : 1;
     }
-    (void)G;
     if (dyn) {
       k_gs_items<OP, NT, RING, false><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
           lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, 0, lv.d_gs_counter, flags,
