@@ -209,6 +209,18 @@ __device__ __forceinline__ void march_prologue(MarchSmem<>& sm, const Band& b, i
 // (blockIdx), so the compiler keeps the 15 C_w of the CTA's macro in uniform
 // registers and feeds them to DFMA directly (no per-node shared loads).
 constexpr int kCMax = 512;
+// k-loop unroll factors (measured on the B200, tools/kbench.py): the residual's
+// f-prefetch rotation and plane-register rotation vanish with 2 (1.66 -> 1.45
+// ms); the apply gains nothing (1.10 either way); the GS pass 3 = its refill
+// period (2.95 -> 2.89 ms).
+#ifndef HHG_RESID_UNROLL
+#define HHG_RESID_UNROLL 2
+#endif
+constexpr int kResidUnroll = HHG_RESID_UNROLL;
+#ifndef HHG_GS_UNROLL
+#define HHG_GS_UNROLL 3
+#endif
+constexpr int kGsUnroll = HHG_GS_UNROLL;
 __constant__ double g_cC[kCMax * 15];
 
 template <int OP, int MODE>
@@ -254,6 +266,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 #pragma unroll
   for (int x = 0; x < FPD; ++x)
     fq[x] = (MODE == kModeResid && q.active && 1 + x <= q.len) ? __ldg(fptr + sm.po[1 + x]) : 0.0;
+#pragma unroll(MODE == kModeResid ? kResidUnroll : 1)
   for (int k = 1; k <= b.kmax; ++k) {
     const int po2 = sm.po[k + 1];
     const double fv = fq[0];
@@ -492,6 +505,7 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
 #ifdef HHG_GS_PROF
   if (threadIdx.x == 0) atomicAdd(&g_gsprof[8], (unsigned long long)(clock64() - _tp0));
 #endif
+#pragma unroll(kGsUnroll)
   for (int s = 0; s < nsteps; ++s) {
     {
       GPROF_T0
