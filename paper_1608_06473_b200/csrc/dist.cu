@@ -334,6 +334,44 @@ hhg_status dist_allreduce_sum(Ctx* c, double* d_scalar) {
   return HHG_OK;
 }
 
+__global__ void k_sum_vec_ranks(int nr, int rank, int64_t n, const double* __restrict__ recv,
+                                double* __restrict__ v) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  int q = 0;
+  for (int p = 0; p < nr; ++p) s += (p == rank) ? v[i] : recv[(int64_t)(q++) * n + i];  // rank order
+  v[i] = s;
+}
+
+// d_vec[0..n) <- elementwise sum over ranks, identical on every rank (NCCL
+// all-reduce; host transport: all-gather + rank-order sum).  Used for vectors
+// whose entries are nonzero on exactly one rank, where every order is exact.
+hhg_status dist_allreduce_vec(Ctx* c, double* d_vec, int64_t n) {
+  if (c->nranks == 1 || n == 0) return HHG_OK;
+  const int nr = c->nranks;
+  if (c->transport == 1) {
+    HHG_NCCL(c, ncclAllReduce(d_vec, d_vec, (size_t)n, ncclDouble, ncclSum, (ncclComm_t)c->nccl_comm, c->stream));
+    return HHG_OK;
+  }
+  double *sendv = nullptr, *recvv = nullptr;
+  HHG_CK(c, cudaMallocAsync((void**)&sendv, (size_t)(nr - 1) * n * sizeof(double), c->stream));
+  HHG_CK(c, cudaMallocAsync((void**)&recvv, (size_t)(nr - 1) * n * sizeof(double), c->stream));
+  for (int q = 0; q < nr - 1; ++q)
+    HHG_CK(c, cudaMemcpyAsync(sendv + (int64_t)q * n, d_vec, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                              c->stream));
+  std::vector<int64_t> sb(nr, n * 8), rb(nr, n * 8);
+  sb[c->rank] = 0;
+  rb[c->rank] = 0;
+  hhg_status st = dist_exchange_bytes(c, sb, sendv, rb, recvv, true);
+  if (st != HHG_OK) return st;
+  k_sum_vec_ranks<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(nr, c->rank, n, recvv, d_vec);
+  HHG_LAUNCHED(c);
+  cudaFreeAsync(sendv, c->stream);
+  cudaFreeAsync(recvv, c->stream);
+  return HHG_OK;
+}
+
 }  // namespace hhg
 
 using namespace hhg;

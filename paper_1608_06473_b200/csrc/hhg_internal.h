@@ -183,6 +183,17 @@ struct Level {
   double* d_fval_cons = nullptr;   // [15][n_frows] exact FEM, affine
   double* d_ftmp = nullptr;        // [n_frows] GS scratch
   int* d_po = nullptr;             // [N+2] plane offsets
+  // replicated coarse solve (coarse.cu): CSR of the exact FEM operator over all
+  // canonical unknowns of the level, identical on every rank
+  bool cg_built = false;
+  int cg_grid = 0;
+  int64_t cg_nnz = 0;
+  int* d_cg_rp = nullptr;          // [n_total+1]
+  int* d_cg_col = nullptr;         // [cg_nnz] canonical ids
+  double* d_cg_val = nullptr;      // [cg_nnz]
+  double* d_cg_vec = nullptr;      // [5][n_total] b, x, r, p, Ap
+  double* d_cg_part = nullptr;     // [3][cg_grid] block partial sums
+  double* d_cg_red = nullptr;      // [nranks][n_total] host-transport allreduce scratch
   std::vector<FaceLP> h_flp;       // host copies (exchange plan)
   std::vector<uint32_t> h_fst;
   std::vector<int> h_fcidx;
@@ -340,6 +351,14 @@ hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out);
 hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* d_out);
 hhg_status zero_dir_slots(Ctx* c, Level& lv, double* out);
 hhg_status lp_sum_copies(Ctx* c, Level& lv, double* v);
+// canonical global vector <-> local layout (ops.cu): owned entries into dglob
+// (0 elsewhere; summed over ranks = the global vector) / every local copy from dglob
+hhg_status gather_owned_dev(Ctx* c, Level& lv, const double* local, double* dglob);
+hhg_status scatter_global_dev(Ctx* c, Level& lv, const double* dglob, double* local);
+// replicated coarse solve (coarse.cu)
+hhg_status coarse_build(Ctx* c, Level& lv);
+hhg_status coarse_solve(Ctx* c, Level& lv, int iters, double* x, const double* b);
+hhg_status dist_allreduce_vec(Ctx* c, double* d_vec, int64_t n);
 
 // Device geometry helpers (fem.cu)
 hhg_status launch_fem_partial(Ctx* c, int L, const uint32_t* d_slots, int64_t n, bool blended,

@@ -868,6 +868,41 @@ extern "C" hhg_status hhg_gs_sweep_lex(hhg_ctx ctx, int L, hhg_op op, double* u,
   return gs_sweep_api(ctx, L, op, u, f, n, true);
 }
 
+namespace hhg {
+
+hhg_status gather_owned_dev(Ctx* c, Level& lv, const double* local, double* dglob) {
+  HHG_CK(c, cudaMemsetAsync(dglob, 0, lv.gi.n_total * sizeof(double), c->stream));
+  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
+  k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, local, dglob, 0);
+  HHG_LAUNCHED(c);
+  if (lv.n_rows) {
+    k_lp_gather<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy,
+                                                            lv.d_row_gid, local, dglob, 0);
+    HHG_LAUNCHED(c);
+  }
+  return face_gather(c, lv, local, dglob, 0);
+}
+
+hhg_status scatter_global_dev(Ctx* c, Level& lv, const double* dglob, double* local) {
+  hhg_status st;
+  HHG_CK(c, cudaMemsetAsync(local, 0, lv.n_local * sizeof(double), c->stream));
+  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_blocks);  // ghost interiors too
+  k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, local, (double*)dglob, 1);
+  HHG_LAUNCHED(c);
+  if (lv.n_rows) {
+    k_lp_gather<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy,
+                                                            lv.d_row_gid, local, (double*)dglob, 1);
+    HHG_LAUNCHED(c);
+  }
+  if ((st = face_gather(c, lv, local, (double*)dglob, 1)) != HHG_OK) return st;
+  if ((st = dist_sync(c, lv, local)) != HHG_OK) return st;
+  return zero_dir(c, lv, local);
+}
+
+}  // namespace hhg
+
+using namespace hhg;
+
 extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local, double* glob) {
   Ctx* c = (Ctx*)ctx;
   if (!c || L < 2 || L > c->L_max || !local || !glob) return HHG_ERR_INVALID;
@@ -881,16 +916,7 @@ extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local,
   double* dglob = glob;
   bool host_glob = !is_device_ptr(glob);
   if (host_glob) HHG_CK(c, cudaMalloc(&dglob, lv.gi.n_total * sizeof(double)));
-  HHG_CK(c, cudaMemsetAsync(dglob, 0, lv.gi.n_total * sizeof(double), c->stream));
-  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
-  k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, sl.dev, dglob, 0);
-  HHG_LAUNCHED(c);
-  if (lv.n_rows) {
-    k_lp_gather<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy,
-                                                            lv.d_row_gid, sl.dev, dglob, 0);
-    HHG_LAUNCHED(c);
-  }
-  if ((st = face_gather(c, lv, sl.dev, dglob, 0)) != HHG_OK) return st;
+  if ((st = gather_owned_dev(c, lv, sl.dev, dglob)) != HHG_OK) return st;
   if (host_glob) {
     HHG_CK(c, cudaMemcpyAsync(glob, dglob, lv.gi.n_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     HHG_CK(c, cudaStreamSynchronize(c->stream));
@@ -916,18 +942,7 @@ extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob,
     HHG_CK(c, cudaMemcpyAsync(tmp, glob, lv.gi.n_total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     dglob = tmp;
   }
-  HHG_CK(c, cudaMemsetAsync(sl.dev, 0, lv.n_local * sizeof(double), c->stream));
-  dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_blocks);  // ghost interiors too
-  k_vol_gather<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_topo, lv.gi, sl.dev, (double*)dglob, 1);
-  HHG_LAUNCHED(c);
-  if (lv.n_rows) {
-    k_lp_gather<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy,
-                                                            lv.d_row_gid, sl.dev, (double*)dglob, 1);
-    HHG_LAUNCHED(c);
-  }
-  if ((st = face_gather(c, lv, sl.dev, (double*)dglob, 1)) != HHG_OK) return st;
-  if ((st = dist_sync(c, lv, sl.dev)) != HHG_OK) return st;
-  if ((st = zero_dir(c, lv, sl.dev)) != HHG_OK) return st;
+  if ((st = scatter_global_dev(c, lv, dglob, sl.dev)) != HHG_OK) return st;
   if ((st = unstage(c, sl, lv.n_local)) != HHG_OK) return st;
   if (tmp) {
     HHG_CK(c, cudaStreamSynchronize(c->stream));

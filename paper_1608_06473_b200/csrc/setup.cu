@@ -584,7 +584,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();

@@ -157,9 +157,21 @@ static hhg_status level_vec(Ctx* c, std::vector<double*>& v, int L) {
   return HHG_OK;
 }
 
+// Coarse solver selection: the replicated CSR solve (coarse.cu, default) or,
+// with HHG_COARSE=ops, CG through the library's operator calls (one apply, three
+// dot products and two updates per iteration) -- the same recurrence.
+static bool coarse_ops() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("HHG_COARSE");
+    v = (e && std::string(e) == "ops") ? 1 : 0;
+  }
+  return v == 1;
+}
+
 // x = A^-1 b by `iters` CG iterations from x = 0 on the exact FEM operator
 // (surrogate at L = 2 is the exact stencil; above, the node-wise FEM operator).
-static hhg_status coarse_cg(Ctx* c, int L, int iters, double* x, const double* b) {
+static hhg_status coarse_cg_ops(Ctx* c, int L, int iters, double* x, const double* b) {
   Level& lv = c->levels[L];
   const int64_t n = lv.n_local;
   const int op = L == 2 ? HHG_OP_SURROGATE : HHG_OP_FEM_ELEMENTWISE;
@@ -222,7 +234,8 @@ static hhg_status prolong_add(Ctx* c, int Lf, const double* uc, double* uf) {
 static hhg_status vcycle_rec(Ctx* c, int L, int Lc, int nu1, int nu2, int cg_iters, int op, int rop, bool lex,
                              double* u, const double* f) {
   hhg_status st;
-  if (L == Lc) return coarse_cg(c, L, cg_iters, u, f);
+  if (L == Lc)
+    return coarse_ops() ? coarse_cg_ops(c, L, cg_iters, u, f) : coarse_solve(c, c->levels[L], cg_iters, u, f);
   Level& lv = c->levels[L];
   for (int s = 0; s < nu1; ++s)
     if ((st = gs_sweep_dev(c, lv, op, u, f, lex)) != HHG_OK) return st;
@@ -289,6 +302,9 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
     if (!c->levels[l].fitted) return set_err(c, HHG_ERR_STATE, "hhg_vcycle: call hhg_fit_surrogates first");
   hhg_status st = ensure_mg(c);
   if (st != HHG_OK) return st;
+  // the coarse matrix is assembled once per level (collective, synchronising:
+  // never inside a graph capture)
+  if (!coarse_ops() && (st = coarse_build(c, c->levels[L_coarse])) != HHG_OK) return st;
   Level& lv = c->levels[L];
   const int64_t n = lv.n_local;
   // host vectors are staged

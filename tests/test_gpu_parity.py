@@ -220,6 +220,30 @@ def test_vcycle_history_matches_oracle(mesh_name, L, cycles):
     assert hist[-1] < 0.1 * hist[0]
 
 
+@functools.lru_cache(maxsize=None)
+def oracle_hierarchy_c(mesh_name, L, Lc):
+    return solvers.Hierarchy(MESHES[mesh_name](), L, Lc, 2)
+
+
+@pytest.mark.parametrize("mesh_name,L,Lc,cycles", [("tet", 3, 3, 1), ("shell60", 3, 3, 1), ("shell60", 4, 3, 2),
+                                                   ("shell120", 4, 3, 1)])
+def test_coarse_solve_level3_matches_oracle(mesh_name, L, Lc, cycles):
+    """The replicated coarse solve (coarse.cu: exact FEM CSR over the canonical
+    ids, all 50 CG iterations in one cooperative kernel) on a level with volume,
+    face, edge and vertex rows: L = Lc is a pure CG solve from zero, L > Lc a
+    V(3,3) cycle on top of it; histories and iterates agree with the oracle's
+    cg on its assembled coarse matrix to 1e-10."""
+    H = oracle_hierarchy_c(mesh_name, L, Lc)
+    num = H.num[L]
+    u0, f = vecs(num, (7, 8))
+    u_ref, hist_ref = H.solve(u0.copy(), f, cycles)
+    ctx = gpu_ctx(mesh_name, L)
+    du, df = to_local(ctx, L, u0), to_local(ctx, L, f)
+    hist = ctx.vcycle(L, du, df, n_cycles=cycles, L_coarse=Lc)
+    assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
+    assert rel(ctx.gather_global(L, du), u_ref) < 1e-10
+
+
 @pytest.mark.parametrize("mesh_name,L,cycles", [("tet", 4, 3), ("shell60", 4, 3)])
 def test_vcycle_double_discretisation_matches_oracle(mesh_name, L, cycles):
     """Double discretisation: surrogate GS smoother, exact
