@@ -12,6 +12,8 @@ import os
 
 import numpy as np
 
+from .partition import partition_rcb  # noqa: F401  (host logic: macro -> rank)
+
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libhhg.so")
 

@@ -351,6 +351,7 @@ hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out);
 hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* d_out);
 hhg_status zero_dir_slots(Ctx* c, Level& lv, double* out);
 hhg_status lp_sum_copies(Ctx* c, Level& lv, double* v);
+hhg_status lp_sync_own_copies(Ctx* c, Level& lv, double* v);
 // canonical global vector <-> local layout (ops.cu): owned entries into dglob
 // (0 elsewhere; summed over ranks = the global vector) / every local copy from dglob
 hhg_status gather_owned_dev(Ctx* c, Level& lv, const double* local, double* dglob);

@@ -226,6 +226,10 @@ static hhg_status prolong_add(Ctx* c, int Lf, const double* uc, double* uf) {
   dim3 grid(nblk((int64_t)(F.N + 1) * (F.N + 2) / 2, 128), (unsigned)c->nt_local);  // fine columns
   k_prolong_add<<<grid, 128, 0, c->stream>>>(F.N, F.S, C.S, F.P, uc, uf);
   HHG_LAUNCHED(c);
+  if (c->nranks > 1) {  // ghost-block copies of this rank's own nodes, then the other ranks' values
+    hhg_status st = lp_sync_own_copies(c, F, uf);
+    if (st != HHG_OK) return st;
+  }
   return dist_sync(c, F, uf);  // ghost-block slots of the other ranks' macros
 }
 

@@ -24,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, mesh_args, L, out_q):
+def _worker(rank, world, port, mesh_args, L, out_q, part="contig"):
     import sys
     sys.path.insert(0, ROOT)
     import torch.distributed as dist
@@ -36,8 +36,11 @@ def _worker(rank, world, port, mesh_args, L, out_q):
     try:
         mesh = synth.shell_mesh(0.55, 1.0, *mesh_args)
         hhg.set_torch_transport(host_only=True)
-        # radial-layer-friendly contiguous split, but not aligned to layers
-        owner = (np.arange(mesh.nt) * world) // mesh.nt
+        if part == "rcb":  # the bench's partition: whole radial columns
+            from paper_1608_06473_b200.partition import partition_rcb
+            owner = partition_rcb(mesh.vertices, mesh.tets, world)
+        else:  # radial-layer-friendly contiguous split, but not aligned to layers
+            owner = (np.arange(mesh.nt) * world) // mesh.nt
         ctx = hhg.Ctx.from_mesh(mesh, L, rank=rank, nranks=world, owner=owner)
         res = {}
         for lev in range(2, L + 1):
@@ -50,16 +53,18 @@ def _worker(rank, world, port, mesh_args, L, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,mesh_args,L", [(2, (0, 2), 4), (3, (0, 1), 3), (2, (1, 1), 3), (4, (2, 2), 2),
-                                                 (8, (2, 4), 2)])
-def test_partition_plan_consistent(world, mesh_args, L):
+@pytest.mark.parametrize("world,mesh_args,L,part", [(2, (0, 2), 4, "contig"), (3, (0, 1), 3, "contig"),
+                                                      (2, (1, 1), 3, "contig"), (4, (2, 2), 2, "contig"),
+                                                      (8, (2, 4), 2, "contig"), (3, (0, 2), 3, "rcb"),
+                                                      (4, (2, 2), 2, "rcb"), (8, (2, 4), 2, "rcb")])
+def test_partition_plan_consistent(world, mesh_args, L, part):
     import torch.multiprocessing as mp
     import __graft_entry__ as ge
     ge.build()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_args, L, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mesh_args, L, q, part)) for r in range(world)]
     for p in procs:
         p.start()
     results = dict(q.get(timeout=600) for _ in range(world))

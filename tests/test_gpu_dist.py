@@ -99,7 +99,7 @@ def test_two_ranks_match_oracle(world, mesh_args, L):
     assert rel(res[0]["u"], u2) < 1e-12
 
 
-def _vworker(rank, world, port, mesh_args, L, cycles, out_q):
+def _vworker(rank, world, port, mesh_args, L, cycles, out_q, part="contig"):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -113,7 +113,8 @@ def _vworker(rank, world, port, mesh_args, L, cycles, out_q):
         torch.cuda.set_device(0)
         mesh = synth.shell_mesh(0.55, 1.0, *mesh_args)
         hhg.set_torch_transport(host_only=False)
-        owner = (np.arange(mesh.nt) * world) // mesh.nt
+        owner = (hhg.partition_rcb(mesh.vertices, mesh.tets, world) if part == "rcb"
+                 else (np.arange(mesh.nt) * world) // mesh.nt)
         ctx = hhg.Ctx.from_mesh(mesh, L, rank=rank, nranks=world, owner=owner)
         ctx.fit(2)
         n_local, n_owned, n_global = ctx.layout(L)
@@ -137,8 +138,10 @@ def _vworker(rank, world, port, mesh_args, L, cycles, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mesh_args,L,cycles", [((0, 2), 4, 3)])
-def test_two_rank_vcycle_matches_oracle(mesh_args, L, cycles):
+@pytest.mark.parametrize("mesh_args,L,cycles,world,part", [((0, 2), 4, 3, 2, "contig"), ((0, 2), 4, 2, 3, "rcb"),
+                                                               ((0, 2), 4, 2, 3, "contig"), ((0, 2), 3, 1, 3, "rcb"),
+                                                               ((0, 2), 3, 1, 2, "rcb")])
+def test_two_rank_vcycle_matches_oracle(mesh_args, L, cycles, world, part):
     """V(3,3) with the macros split over 2 ranks (restriction partials of
     shared coarse nodes summed across ranks, prolongation re-synced): residual
     history and iterate agree with the single-process oracle to 1e-10."""
@@ -146,8 +149,8 @@ def test_two_rank_vcycle_matches_oracle(mesh_args, L, cycles):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    world = 2
-    procs = [ctx.Process(target=_vworker, args=(r, world, port, mesh_args, L, cycles, q)) for r in range(world)]
+    procs = [ctx.Process(target=_vworker, args=(r, world, port, mesh_args, L, cycles, q, part))
+             for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=900) for _ in range(world))
