@@ -705,22 +705,13 @@ hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* 
   return dist_allreduce_sum(c, d_out);
 }
 
-// every copy of an owned lower-primitive row <- its first (owner-macro) copy
-__global__ void k_lp_copysync(int64_t n_rows, const uint64_t* __restrict__ cp, const uint32_t* __restrict__ copy,
-                              double* __restrict__ v) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n_rows) return;
-  const double x = v[copy[cp[r]]];
-  for (uint64_t e = cp[r] + 1; e < cp[r + 1]; ++e) v[copy[e]] = x;
-}
-
 // Multi-rank: a kernel that updates only the local blocks (prolongation)
 // leaves the ghost-block copies of this rank's OWN lower-primitive nodes stale
 // (no peer sends them: the rank is their owner), and stored rows may read
 // them.  Refresh them from the owner-macro copy.
 hhg_status lp_sync_own_copies(Ctx* c, Level& lv, double* v) {
   if (lv.n_rows) {
-    k_lp_copysync<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy, v);
+    k_lp_sync<<<nblk(lv.n_rows, 128), 128, 0, c->stream>>>(lv.n_rows, lv.d_copy_ptr, lv.d_copy, v);
     HHG_LAUNCHED(c);
   }
   return face_sync(c, lv, v);
