@@ -104,6 +104,10 @@ __global__ void k_coarse_lp_coo(int64_t n_rows, int64_t S, const uint64_t* __res
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 constexpr int kCgThreads = 256;
+#ifndef HHG_CG_ROWS
+#define HHG_CG_ROWS 1
+#endif
+constexpr int kCgRows = HHG_CG_ROWS;  // rows per thread (grid sizing)
 
 // sum of the grid's block partials, fixed order (warp 0), broadcast to the block
 __device__ __forceinline__ double grid_total(const double* part, int nparts, double* sh) {
@@ -161,8 +165,21 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_coop(int64_t n, const int* __
   for (int it = 0; it < iters; ++it) {
     acc = 0.0;
     for (int64_t i = t0; i < n; i += nth) {
+      // row in CSR order (one fma chain); the gathers of 4 entries are issued
+      // together (the loop is L2-latency-bound otherwise)
       double s = 0.0;
-      for (int e = rp[i]; e < rp[i + 1]; ++e) s = fma(val[e], p[col[e]], s);
+      int e = rp[i];
+      const int e1 = rp[i + 1];
+      for (; e + 4 <= e1; e += 4) {
+        const int c0 = col[e], c1 = col[e + 1], c2 = col[e + 2], c3 = col[e + 3];
+        const double v0 = val[e], v1 = val[e + 1], v2 = val[e + 2], v3 = val[e + 3];
+        const double p0 = p[c0], p1 = p[c1], p2 = p[c2], p3 = p[c3];
+        s = fma(v0, p0, s);
+        s = fma(v1, p1, s);
+        s = fma(v2, p2, s);
+        s = fma(v3, p3, s);
+      }
+      for (; e < e1; ++e) s = fma(val[e], p[col[e]], s);
       Ap[i] = s;
       acc = fma(p[i], s, acc);
     }
@@ -275,9 +292,11 @@ hhg_status coarse_build(Ctx* c, Level& lv) {
   HHG_CK(c, cudaGetDevice(&dev));
   HHG_CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
   HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_coop, kCgThreads, 0));
-  // ~8 rows per thread: grid barriers dominate below that
+  // one row per thread while the grid stays co-resident (the SpMV rows are
+  // L2-latency-bound; measured: 8 rows per thread, 3 CTAs at L = 2 on the
+  // 480-macro shell, 1.83 ms for 50 iterations)
   lv.cg_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)nsm * std::max(per_sm, 1),
-                                                           (n + 8 * kCgThreads - 1) / (8 * kCgThreads)));
+                                                           (n + kCgRows * kCgThreads - 1) / (kCgRows * kCgThreads)));
   HHG_CK(c, cudaMalloc(&lv.d_cg_part, 3 * lv.cg_grid * sizeof(double)));
   lv.cg_built = true;
   return HHG_OK;

@@ -2,6 +2,7 @@
 import os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch, paper_1608_06473_b200 as hhg, synth
+if os.environ.get("KB_LIB"): hhg.LIB_PATH = os.path.abspath(os.environ["KB_LIB"])
 m = synth.shell_mesh(0.55, 1.0, 1, 2); L = 7
 ctx = hhg.Ctx.from_mesh(m, L); ctx.fit(2)
 nl, no, ng = ctx.layout(L)
