@@ -312,3 +312,21 @@ def test_surrogate_faces_operator_matches_oracle(mesh_name, L):
     ug = du.clone()
     ctx.gs_sweep(L, ug, df, 1, op="surrogate_faces")
     assert rel(ctx.gather_global(L, ug), solvers.GS(Lf, num).sweep(u.copy(), f, 1)) < TOL
+
+
+@pytest.mark.parametrize("mesh_name,L", [("shell60", 4)])
+def test_vcycle_graph_replay_matches_eager(mesh_name, L, monkeypatch):
+    """HHG_VCYCLE_GRAPH=1 (cycles after the first replay one captured CUDA
+    graph, the cooperative coarse-CG kernel included) gives bit-identical
+    residual histories and iterates to the eager launches."""
+    H = oracle_hierarchy(mesh_name, L)
+    u0, f = vecs(H.num[L], (7, 8))
+    ctx = gpu_ctx(mesh_name, L)
+    du, df = to_local(ctx, L, u0), to_local(ctx, L, f)
+    hist_e = ctx.vcycle(L, du, df, n_cycles=3)
+    ue = ctx.gather_global(L, du)
+    monkeypatch.setenv("HHG_VCYCLE_GRAPH", "1")
+    du2 = to_local(ctx, L, u0)
+    hist_g = ctx.vcycle(L, du2, df, n_cycles=3)
+    assert np.array_equal(hist_g, hist_e), (hist_g, hist_e)
+    assert np.array_equal(ctx.gather_global(L, du2), ue)
