@@ -171,19 +171,21 @@ __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, co
   }
 }
 
-__global__ void k_face_write(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, const FaceLP* __restrict__ flp,
-                             const uint32_t* __restrict__ fst, const int* __restrict__ po, int64_t n_faces,
-                             const double* __restrict__ tmp, double* __restrict__ u) {
+// near-edge rows of one colour step: tmp -> both copies (ne = the colour's
+// near-edge q per mode z, `len` each)
+__global__ void k_face_write(int N, int64_t S, int64_t nfi, int len, const int* __restrict__ ne,
+                             const FaceLP* __restrict__ flp, const uint32_t* __restrict__ fst,
+                             const int* __restrict__ po, int64_t n_faces, const double* __restrict__ tmp,
+                             double* __restrict__ u) {
   __shared__ int po_s[260];
   load_po(po_s, po, N);
   const int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t fc = x / nfc;
+  const int64_t fc = x / len;
   if (fc >= n_faces) return;
-  const int64_t q = q0 + (x - fc * nfc);
   const FaceLP& F = flp[fc];
+  const int64_t q = ne[F.z * len + (x - fc * len)];
   const uint32_t st = fst[F.z * nfi + q];
   const int s = st & 0xffff, t = st >> 16;
-  if (face_inner(N, s, t)) return;  // updated in place by k_face_gs
   const FaceNode a = face_node(F.lA, N, s, t);
   const double v = tmp[fc * nfi + q];
   u[fslot(F.TA, S, po_s, a.i, a.j, a.k)] = v;
@@ -273,9 +275,12 @@ hhg_status face_gs_step(Ctx* c, Level& lv, int op, int colour, double* u, const 
   k_face_gs<<<nblk(n, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, nfc, lv.fcol[colour], lv.d_flp, lv.d_fst,
                                                  lv.d_po, lv.n_frows, val, u, f, lv.d_ftmp, fcoef, lv.q);
   HHG_LAUNCHED(c);
-  k_face_write<<<nblk(n, 128), 128, 0, c->stream>>>(lv.N, lv.S, lv.gi.nfi, nfc, lv.fcol[colour], lv.d_flp,
-                                                    lv.d_fst, lv.d_po, lv.n_flp, lv.d_ftmp, u);
-  HHG_LAUNCHED(c);
+  const int len = lv.fne_len[colour];
+  if (len > 0) {
+    k_face_write<<<nblk((int64_t)len * lv.n_flp, 128), 128, 0, c->stream>>>(
+        lv.N, lv.S, lv.gi.nfi, len, lv.d_fne[colour], lv.d_flp, lv.d_fst, lv.d_po, lv.n_flp, lv.d_ftmp, u);
+    HHG_LAUNCHED(c);
+  }
   return HHG_OK;
 }
 

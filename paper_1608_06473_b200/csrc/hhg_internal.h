@@ -175,6 +175,8 @@ struct Level {
   // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order
   int64_t n_flp = 0, n_frows = 0;
   int fcol[4] = {0, 0, 0, 0};      // colour offsets of q ((s+2t) mod 3 = 0,1,2)
+  int fne_len[3] = {0, 0, 0};      // near-edge rows per face and colour (same for every mode z)
+  int* d_fne[3] = {nullptr, nullptr, nullptr};  // [colour][3 modes z][fne_len] q of near-edge rows
   FaceLP* d_flp = nullptr;
   uint32_t* d_fst = nullptr;       // [3][nfi] s | t << 16 for q, per row mode z
   int* d_fcidx = nullptr;          // [3][nfi] canonical in-face index of q

@@ -188,6 +188,21 @@ static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
   if ((st = up(lv.d_fst, fst)) != HHG_OK) return st;
   if ((st = up(lv.d_fcidx, fcidx)) != HHG_OK) return st;
   if ((st = up(lv.d_po, po)) != HHG_OK) return st;
+  // near-edge rows (k_face_gs writes them through tmp; k_face_write visits only these)
+  for (int col = 0; col < 3; ++col) {
+    std::vector<int> ne[3];
+    for (int z = 0; z < 3; ++z)
+      for (int q = lv.fcol[col]; q < lv.fcol[col + 1]; ++q) {
+        const int s = fst[z * nfi + q] & 0xffff, t = fst[z * nfi + q] >> 16;
+        if (!(s >= 2 && t >= 2 && s + t <= N - 2)) ne[z].push_back(q);
+      }
+    if (ne[0].size() != ne[1].size() || ne[0].size() != ne[2].size())
+      return set_err(c, HHG_ERR_STATE, "near-edge face rows differ between modes");
+    std::vector<int> all;
+    for (int z = 0; z < 3; ++z) all.insert(all.end(), ne[z].begin(), ne[z].end());
+    lv.fne_len[col] = (int)ne[0].size();
+    if ((st = up(lv.d_fne[col], all)) != HHG_OK) return st;
+  }
   const size_t nv = (size_t)std::max<int64_t>(lv.n_frows, 1);
   HHG_CK(c, cudaMalloc(&lv.d_fval, 15 * nv * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_fval_cons, 15 * nv * sizeof(double)));
@@ -584,7 +599,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red, lv.d_fne[0], lv.d_fne[1], lv.d_fne[2]};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
