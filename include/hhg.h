@@ -72,7 +72,11 @@ typedef enum {
   HHG_ERR_MESH = 2,     /* degenerate tet, non-conforming / over-shared face,
                            |x_v| != r_v beyond 1e-12 relative */
   HHG_ERR_FIT = 3,      /* rank-deficient sampling matrix */
-  HHG_ERR_NUMERIC = 4,  /* non-positive centre weight */
+  HHG_ERR_NUMERIC = 4,  /* non-positive surrogate centre weight (the GS update
+                           divides by it): raised by
+                           hhg_fit_surrogates / hhg_fit_from_samples (the fit is
+                           still installed: apply and residual work) and by
+                           every later hhg_gs_sweep / hhg_vcycle on that level */
   HHG_ERR_DIVERGED = 5, /* V-cycle residual grew 3 cycles in a row */
   HHG_ERR_CUDA = 6,
   HHG_ERR_NCCL = 7,
@@ -125,8 +129,27 @@ hhg_status hhg_setup_macro_mesh(const double* vertices, const double* vertex_rad
  * set S_l = M_m(l,j), m(l,j) = min{l, max{1,j}} (LSQP) or the 10 IPOLY points
  * (q = 2 only), then a = A^+ b with A^+ from one Householder QR per level.
  * Level 2 (l = 0) uses its exact stencil.  q in 0..4 (full rank, PAPER.md:
- * 530-534).  Errors: HHG_ERR_INVALID, HHG_ERR_FIT, HHG_ERR_CUDA. */
+ * 530-534).  After the fit every interior node's centre weight (and every
+ * face node's, for the face surrogates) is evaluated once; a non-positive one
+ * returns HHG_ERR_NUMERIC with the fit installed.  Errors: HHG_ERR_INVALID,
+ * HHG_ERR_FIT, HHG_ERR_NUMERIC, HHG_ERR_CUDA. */
 hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method method, int sampling_j);
+
+/* TEST EXPORTS of the fit.
+ * hhg_sample_nodes: the sampling set of level L (3 <= L <= L_max) that
+ *   hhg_fit_surrogates uses for (method, sampling_j) -- LSQP: the interior
+ *   nodes of the 2^(m+2) lattice, m = min(L-2, max(1, j)), at level-L indices
+ *   x 2^(L-2-m); IPOLY: the 10 points of PAPER.md:490-499 --
+ *   as ijk[n][3] (host, caller-owned; NULL to query n only) in fit order.
+ * hhg_fit_from_samples: fit level L from the caller's samples instead of the
+ *   exact FEM stencils: samples[nt_local][n][15] (host or device, fp64; sample
+ *   order of hhg_sample_nodes, direction order above), a_w = A^+ b_w as in
+ *   hhg_fit_surrogates.  Replaces level L's volume coefficients only (its face
+ *   surrogates are dropped: HHG_OP_SURROGATE_FACES is then refused on L).
+ *   Errors: HHG_ERR_INVALID, HHG_ERR_FIT, HHG_ERR_NUMERIC (see above). */
+hhg_status hhg_sample_nodes(hhg_ctx ctx, int L, hhg_fit_method method, int sampling_j, int32_t* ijk, int64_t* n);
+hhg_status hhg_fit_from_samples(hhg_ctx ctx, int L, int q, hhg_fit_method method, int sampling_j,
+                                const double* samples);
 
 /* Sizes at level L: doubles of a local vector (incl. copies and padding),
  * owned unknowns (each unknown counted on exactly one rank), and the length

@@ -90,20 +90,23 @@ def volume_stencils(mesh, T: int, ijk: np.ndarray, N: int, blended=True) -> np.n
     return out
 
 
-def fem_row(mesh, num: Numbering, gid: int, blended=True, macros=None) -> dict:
+def fem_row(mesh, num: Numbering, gid: int, blended=True, macros=None, locs=None) -> dict:
     """Row `gid` of the global FEM matrix (no BC) by node-wise assembly over
     every fine tet of every macro containing the node: {gid_J: value}.
     `macros` (optional) lists the candidate macros to search, ascending (a
-    superset of those containing the node); the sum is the same."""
+    superset of those containing the node); the sum is the same.  `locs`
+    (optional) gives the node's (macro, ijk) positions directly (e.g.
+    `num.locate(gid)`), ascending macro order, instead of the search."""
     N = num.N
-    lat = lattice_ijk(N)
     row = {}
-    for T in (range(mesh.nt) if macros is None else macros):
-        g = num.gids(T, lat)
-        hit = np.nonzero(g == gid)[0]
-        if len(hit) == 0:
-            continue
-        ijk = lat[hit[0]]
+    if locs is None:
+        lat = lattice_ijk(N)
+        locs = []
+        for T in (range(mesh.nt) if macros is None else macros):
+            hit = np.nonzero(num.gids(T, lat) == gid)[0]
+            if len(hit):
+                locs.append((T, lat[hit[0]]))
+    for T, ijk in locs:
         for tet in incident_kuhn_tets(ijk, N, inside_only=True):
             P = node_coords(mesh, T, tet, N, blended)
             K = local_stiffness(P)

@@ -254,6 +254,69 @@ class Numbering:
             out[m4] = self.base_v + T * self.nvi + v
         return out
 
+    def _face_st(self, idx):
+        """(s, t) of in-face index idx = (t-1)(N-1) - (t-1)t/2 + (s-1)."""
+        N = self.N
+        t = 1
+        while idx >= N - 1 - t:
+            idx -= N - 1 - t
+            t += 1
+        return idx + 1, t
+
+    def locate(self, gid: int):
+        """Every (macro T, lattice ijk) holding node `gid`, ascending T: the
+        inverse of `gids` (vertex: gid; edge (a<b): node a + (m/N)(b-a); face
+        (a<b<c): a + (s/N)(b-a) + (t/N)(c-a); volume: (T, k, j, i) order)."""
+        N = self.N
+        gid = int(gid)
+        if gid >= self.base_v:
+            T, v = divmod(gid - self.base_v, self.nvi)
+            if not hasattr(self, "_inter"):
+                self._inter = interior_ijk(N)
+            return [(int(T), self._inter[v].copy())]
+        if gid >= self.base_f:
+            fid, idx = divmod(gid - self.base_f, self.nfi)
+            a, b, c = (int(x) for x in self.faces[fid])
+            s, t = self._face_st(idx)
+            wts = {a: N - s - t, b: s, c: t}
+        elif gid >= self.base_e:
+            eid, m1 = divmod(gid - self.base_e, N - 1)
+            a, b = (int(x) for x in self.edges[eid])
+            wts = {a: N - (m1 + 1), b: m1 + 1}
+        else:
+            wts = {gid: N}
+        if not hasattr(self, "_vmacros"):
+            self._vmacros = [[] for _ in range(self.mesh.nv)]
+            for T, tv in enumerate(self.mesh.tets):
+                for v in tv:
+                    self._vmacros[int(v)].append(T)
+        out = []
+        for T in self._vmacros[next(iter(wts))]:
+            tv = [int(v) for v in self.mesh.tets[T]]
+            if all(v in tv for v in wts):
+                w = [wts.get(v, 0) for v in tv]
+                out.append((T, np.array(w[1:4], dtype=np.int64)))
+        return out
+
+    def step_of(self, gid: int) -> int:
+        """Index of the GS class step (in `gs_steps` order) that updates node
+        `gid`: 0 vertices, 1-2 edge colours, 3-5 face colours, 6-9 volume
+        colours; -1 for Dirichlet nodes (never updated)."""
+        gid = int(gid)
+        if self.dirichlet_mask[gid]:
+            return -1
+        N = self.N
+        if gid < self.base_e:
+            return 0
+        if gid < self.base_f:
+            m = (gid - self.base_e) % (N - 1) + 1
+            return 1 + m % 2
+        if gid < self.base_v:
+            s, t = self._face_st((gid - self.base_f) % self.nfi)
+            return 3 + (s + 2 * t) % 3
+        i, j, k = self.locate(gid)[0][1]
+        return 6 + int(i + 2 * j + 3 * k) % 4
+
     def node_class(self, gid):
         gid = np.asarray(gid)
         return np.where(gid < self.base_e, 0, np.where(gid < self.base_f, 1,

@@ -43,6 +43,8 @@ def lib():
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.hhg_setup_macro_mesh.argtypes = [P, P, I64, P, I64, P, I32, P, I32, I32, P, P, ctypes.POINTER(P)]
     L.hhg_fit_surrogates.argtypes = [P, I32, I32, I32]
+    L.hhg_sample_nodes.argtypes = [P, I32, I32, I32, P, ctypes.POINTER(I64)]
+    L.hhg_fit_from_samples.argtypes = [P, I32, I32, I32, I32, P]
     L.hhg_vector_layout.argtypes = [P, I32, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.hhg_apply.argtypes = [P, I32, I32, P, P]
     L.hhg_residual.argtypes = [P, I32, I32, P, P, P, P]
@@ -217,6 +219,19 @@ class Ctx:
     # ------------------------------------------------------------------
     def fit(self, q=2, method="lsqp", j=2):
         self._check(self._lib.hhg_fit_surrogates(self.h, q, FIT[method], j))
+
+    def sample_nodes(self, L, method="lsqp", j=2):
+        """Sampling set of level L used by the fit (test export), [n, 3] int32."""
+        n = ctypes.c_int64()
+        self._check(self._lib.hhg_sample_nodes(self.h, L, FIT[method], j, None, ctypes.byref(n)))
+        out = np.zeros((n.value, 3), dtype=np.int32)
+        self._check(self._lib.hhg_sample_nodes(self.h, L, FIT[method], j, out.ctypes.data, ctypes.byref(n)))
+        return out
+
+    def fit_from_samples(self, L, samples, q=2, method="lsqp", j=2):
+        """Fit level L from planted samples [nt_local, n, 15] (test export)."""
+        s = np.ascontiguousarray(samples, dtype=np.float64)
+        self._check(self._lib.hhg_fit_from_samples(self.h, L, q, FIT[method], j, s.ctypes.data))
 
     def layout(self, L):
         a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

@@ -204,11 +204,18 @@ __global__ void __launch_bounds__(kCgThreads) k_cg_coop(int64_t n, const int* __
   }
 }
 
+// The replicated solve holds the level's whole CSR matrix on every rank (int32
+// row pointers and columns) and sorts its COO on the host: only for levels of
+// at most kCoarseMaxUnknowns unknowns (~15 entries per row: <= 63 M entries,
+// 1.5 GB of COO); larger coarse levels use the CG through the operator calls
+// (vcycle.cu::coarse_cg_ops).
+bool coarse_replicable(const Level& lv) { return lv.gi.n_total <= kCoarseMaxUnknowns; }
+
 hhg_status coarse_build(Ctx* c, Level& lv) {
   if (lv.cg_built) return HHG_OK;
   const GidInfo& gi = lv.gi;
   const int64_t n = gi.n_total;
-  if (n >= (1ll << 31)) return set_err(c, HHG_ERR_INVALID, "coarse level too large for the replicated solve");
+  if (!coarse_replicable(lv)) return set_err(c, HHG_ERR_INVALID, "coarse level too large for the replicated solve");
   const int64_t cap = c->nt_local * gi.nvi * 15 + lv.n_frows * 15 + lv.nnz;
   CooEntry* d_coo = nullptr;
   unsigned long long* d_cnt = nullptr;
@@ -233,7 +240,7 @@ hhg_status coarse_build(Ctx* c, Level& lv) {
   }
   unsigned long long cnt = 0;
   HHG_CK(c, cudaMemcpyAsync(&cnt, d_cnt, sizeof(cnt), cudaMemcpyDeviceToHost, c->stream));
-  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
   if ((int64_t)cnt > cap) return set_err(c, HHG_ERR_STATE, "coarse COO overflow");
   std::vector<CooEntry> coo(cnt);
   HHG_CK(c, cudaMemcpy(coo.data(), d_coo, cnt * sizeof(CooEntry), cudaMemcpyDeviceToHost));
@@ -259,6 +266,8 @@ hhg_status coarse_build(Ctx* c, Level& lv) {
     if (st != HHG_OK) return st;
     coo.insert(coo.end(), recvv.begin(), recvv.end());
   }
+  if ((int64_t)coo.size() >= (1ll << 31) - 1)
+    return set_err(c, HHG_ERR_INVALID, "coarse matrix too large for 32-bit CSR indices");
   std::sort(coo.begin(), coo.end(), [](const CooEntry& a, const CooEntry& b) {
     return a.row != b.row ? a.row < b.row : a.col < b.col;
   });

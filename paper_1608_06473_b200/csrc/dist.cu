@@ -14,7 +14,9 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cstring>
+#include <thread>
 
 #include "fem_device.cuh"
 #include "hhg_internal.h"
@@ -55,6 +57,37 @@ hhg_status dist_init_transport(Ctx* c, const void* nccl_unique_id) {
   return HHG_OK;
 }
 
+// Wait for the ctx stream; with the NCCL transport, poll the communicator's
+// asynchronous error state while waiting and abort it (sticky HHG_ERR_NCCL)
+// on an error or after HHG_NCCL_TIMEOUT_S seconds (default 600) without
+// progress -- a peer that died must not hang this rank forever.
+hhg_status ctx_sync(Ctx* c) {
+  if (c->transport != 1 || !c->nccl_comm) {
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    return HHG_OK;
+  }
+  const char* e = getenv("HHG_NCCL_TIMEOUT_S");
+  const double limit = e ? atof(e) : 600.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    cudaError_t q = cudaStreamQuery(c->stream);
+    if (q == cudaSuccess) return HHG_OK;
+    if (q != cudaErrorNotReady) return check_cuda(c, q, "cudaStreamQuery");
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError((ncclComm_t)c->nccl_comm, &ar);
+    const double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ar != ncclSuccess && ar != ncclInProgress) || dt > limit) {
+      ncclCommAbort((ncclComm_t)c->nccl_comm);
+      c->nccl_comm = nullptr;
+      c->poisoned = true;
+      return set_err(c, HHG_ERR_NCCL, ar != ncclSuccess && ar != ncclInProgress
+                                          ? std::string("NCCL async error: ") + ncclGetErrorString(ar)
+                                          : std::string("NCCL wait timed out"));
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
 void dist_destroy(Ctx* c) {
   if (c->nccl_comm) ncclCommDestroy((ncclComm_t)c->nccl_comm);
   c->nccl_comm = nullptr;
@@ -75,7 +108,8 @@ hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& sb, const voi
     if (!device) {  // setup-time host data
       HHG_CK(c, cudaMalloc(&ds, std::max<int64_t>(ts, 1)));
       HHG_CK(c, cudaMalloc(&dr, std::max<int64_t>(tr, 1)));
-      HHG_CK(c, cudaMemcpy(ds, send, ts, cudaMemcpyHostToDevice));
+      // stream-ordered before the sends (the ctx stream may be a non-blocking stream)
+      HHG_CK(c, cudaMemcpyAsync(ds, send, ts, cudaMemcpyHostToDevice, c->stream));
       s = (const char*)ds;
       r = (char*)dr;
     }
@@ -90,7 +124,7 @@ hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& sb, const voi
     HHG_NCCL(c, ncclGroupEnd());
     if (!device) {
       HHG_CK(c, cudaMemcpyAsync(recv, dr, tr, cudaMemcpyDeviceToHost, c->stream));
-      HHG_CK(c, cudaStreamSynchronize(c->stream));
+      { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
       cudaFree(ds);
       cudaFree(dr);
     }

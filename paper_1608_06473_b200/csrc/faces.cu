@@ -66,6 +66,27 @@ __device__ __forceinline__ double face_poly(const double* __restrict__ cf, int q
   return v;
 }
 
+// flag |= 2 if a fitted face surrogate's centre weight (entry 0) is <= 0 (or
+// NaN) at a face node (the face GS class steps divide by it).
+__global__ void k_face_check_centre(int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
+                                    const uint32_t* __restrict__ fst, const double* __restrict__ fcoef, int fq,
+                                    int* __restrict__ flag) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_frows) return;
+  const int64_t fc = r / nfi;
+  const uint32_t st = fst[flp[fc].z * nfi + (r - fc * nfi)];
+  const int nfc = (fq + 1) * (fq + 2) / 2;
+  if (!(face_poly(fcoef + fc * 15 * nfc, fq, st & 0xffff, st >> 16) > 0.0)) atomicOr(flag, 2);
+}
+
+hhg_status face_centre_check(Ctx* c, Level& lv, int* d_flag) {
+  if (!lv.d_fcoef || lv.n_frows == 0) return HHG_OK;
+  k_face_check_centre<<<(unsigned)((lv.n_frows + 127) / 128), 128, 0, c->stream>>>(
+      lv.gi.nfi, lv.n_frows, lv.d_flp, lv.d_fst, lv.d_fcoef, lv.q, d_flag);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
 // mode: kModeApply / kModeResid (vol_kernels.cuh values 0 / 1)
 __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
                              const uint32_t* __restrict__ fst, const int* __restrict__ po,

@@ -29,11 +29,11 @@
 // definition (fem.assemble); the order of the sums differs.
 #pragma once
 #include "fem_device.cuh"
-#include "femmarch.cuh"
 #include "march.cuh"
 
 namespace hhg {
 
+constexpr int kFPosPerThread = 3;  // ring columns per thread whose positions it computes
 constexpr int kEwRing = 6;  // u plane slots (slab k0 reads planes k0, k0+1)
 
 // corner index a | b<<1 | c<<2; the 6 Kuhn tets (step orders XYZ, XZY, YXZ,

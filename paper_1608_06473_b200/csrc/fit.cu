@@ -12,6 +12,7 @@
 
 #include "fem_device.cuh"
 #include "hhg_internal.h"
+#include "vol_kernels.cuh"
 
 namespace hhg {
 
@@ -174,116 +175,221 @@ __global__ void k_exact_const(const double* __restrict__ geo, int N, int mq, boo
   }
 }
 
+// Sampling set of level L (lattice indices, [n][3]): LSQP S_l = M_m(l,j)
+// embedded at level l (index x 2^(l-m), reading R10), or the
+// 10 IPOLY points.
+static std::vector<int> sample_set(int L, hhg_fit_method method, int sampling_j) {
+  std::vector<int> smp;
+  const int l = L - 2;
+  if (method == HHG_FIT_IPOLY) {
+    const int a = (1 << (l + 2)) - 3, b = (1 << (l + 1)) - 1;
+    const int pts[10][3] = {{1, 1, 1}, {1, 1, a}, {1, a, 1}, {a, 1, 1}, {1, 1, b},
+                            {1, b, 1}, {b, 1, 1}, {1, b, b}, {b, 1, b}, {b, b, 1}};
+    for (auto& p : pts) smp.insert(smp.end(), p, p + 3);
+    return smp;
+  }
+  const int m = std::min(l, std::max(1, sampling_j));
+  const int Nm = 1 << (m + 2), sc = 1 << (l - m);
+  for (int k = 1; k < Nm; ++k)
+    for (int j = 1; j < Nm - k; ++j)
+      for (int i = 1; i < Nm - k - j; ++i) {
+        smp.push_back(i * sc);
+        smp.push_back(j * sc);
+        smp.push_back(k * sc);
+      }
+  return smp;
+}
+
+// flag |= 1 if the surrogate centre weight s_mc(i,j,k) <= 0 (or NaN) at an
+// interior node: the GS update divides by it (eq. iteration-scheme,
+// PAPER.md:1306-1315).  Evaluated like node_weights (vol_kernels.cuh).
+__global__ void k_check_centre(int N, int64_t P, const double* __restrict__ coef, int mq, int* __restrict__ flag) {
+  const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t T = blockIdx.y;
+  if (p >= P) return;
+  int i, j, k;
+  decode_pos(N, p, i, j, k);
+  if (i < 1 || j < 1 || k < 1 || i + j + k > N - 1) return;
+  double s[15];
+  node_weights(HHG_OP_SURROGATE, N, i, j, k, nullptr, coef + T * 15 * mq, mq, nullptr, false, s);
+  if (!(s[kMC] > 0.0)) atomicOr(flag, 1);
+}
+
+static hhg_status check_centre(Ctx* c, Level& lv) {
+  if (!c->d_flag) HHG_CK(c, cudaMalloc(&c->d_flag, sizeof(int)));
+  HHG_CK(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  if (c->nt_local > 0) {
+    dim3 g((unsigned)((lv.P + 127) / 128), (unsigned)c->nt_local);
+    k_check_centre<<<g, 128, 0, c->stream>>>(lv.N, lv.P, lv.d_coef, lv.mq, c->d_flag);
+    HHG_LAUNCHED(c);
+  }
+  hhg_status st = face_centre_check(c, lv, c->d_flag + 0);
+  if (st != HHG_OK) return st;
+  int h = 0;
+  HHG_CK(c, cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  lv.centre_bad = (h & 1) != 0;
+  lv.fcentre_bad = (h & 2) != 0;
+  return HHG_OK;
+}
+
+// q <= 2: the march kernels read coefficients zero-padded to the q = 2 layout
+// (the degree-major exponent list of q is a prefix of that of q = 2).
+static hhg_status make_coef10(Ctx* c, Level& lv, int q, int mq) {
+  if (lv.d_coef10) cudaFree(lv.d_coef10);
+  lv.d_coef10 = nullptr;
+  if (lv.d_cC) cudaFree(lv.d_cC);  // derived from d_coef10 on first use (ops.cu)
+  lv.d_cC = nullptr;
+  if (q > 2) return HHG_OK;
+  HHG_CK(c, cudaMalloc(&lv.d_coef10, c->nt_local * 150 * sizeof(double)));
+  HHG_CK(c, cudaMemsetAsync(lv.d_coef10, 0, c->nt_local * 150 * sizeof(double), c->stream));
+  HHG_CK(c, cudaMemcpy2DAsync(lv.d_coef10, 10 * sizeof(double), lv.d_coef, mq * sizeof(double),
+                              mq * sizeof(double), c->nt_local * 15, cudaMemcpyDeviceToDevice, c->stream));
+  return HHG_OK;
+}
+
+// Fit one level L >= 3: coefficients = A^+ B with B the exact FEM stencils at
+// the sampling set (d_samples = nullptr) or the caller's planted samples
+// (d_samples [nt_local][n][15], hhg_fit_from_samples).
+static hhg_status fit_level(Ctx* c, Level& lv, int L, int q, hhg_fit_method method, int sampling_j,
+                            const double* d_samples) {
+  const int N = lv.N;
+  const int mq = n_coeffs(q);
+  std::vector<int> el, em, en;
+  exponents(q, el, em, en);
+  const std::vector<int> smp = sample_set(L, method, sampling_j);
+  const int64_t ns = (int64_t)smp.size() / 3;
+  if (ns < mq) return set_err(c, HHG_ERR_FIT, "fewer sampling points than coefficients");
+  std::vector<double> A(ns * mq);
+  for (int64_t s = 0; s < ns; ++s)
+    for (int cc = 0; cc < mq; ++cc)
+      A[s * mq + cc] = std::pow((double)smp[3 * s] / N, el[cc]) * std::pow((double)smp[3 * s + 1] / N, em[cc]) *
+                       std::pow((double)smp[3 * s + 2] / N, en[cc]);
+  std::vector<double> pinv;
+  if (!pinv_qr(A, ns, mq, pinv))
+    return set_err(c, HHG_ERR_FIT, "rank-deficient sampling matrix at level " + std::to_string(L));
+  // index-unit scaling: x = i/N => a_lmn / N^(l+m+n) (exact powers of two)
+  std::vector<double> scale(mq);
+  for (int cc = 0; cc < mq; ++cc) scale[cc] = std::ldexp(1.0, -L * (el[cc] + em[cc] + en[cc]));
+  if (lv.d_coef) cudaFree(lv.d_coef);
+  lv.d_coef = nullptr;
+  HHG_CK(c, cudaMalloc(&lv.d_coef, c->nt_local * 15 * mq * sizeof(double)));
+  lv.q = q;
+  lv.mq = mq;
+  int* d_smp;
+  double *d_pinv, *d_B = nullptr, *d_scale;
+  HHG_CK(c, cudaMalloc(&d_smp, smp.size() * sizeof(int)));
+  HHG_CK(c, cudaMalloc(&d_pinv, pinv.size() * sizeof(double)));
+  HHG_CK(c, cudaMalloc(&d_scale, mq * sizeof(double)));
+  HHG_CK(c, cudaMemcpyAsync(d_smp, smp.data(), smp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  HHG_CK(c, cudaMemcpyAsync(d_pinv, pinv.data(), pinv.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  HHG_CK(c, cudaMemcpyAsync(d_scale, scale.data(), mq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  if (!d_samples) {
+    HHG_CK(c, cudaMalloc(&d_B, c->nt_local * ns * 15 * sizeof(double)));
+    dim3 g1((unsigned)((ns + 127) / 128), (unsigned)c->nt_local);
+    k_sample_stencils<<<g1, 128, 0, c->stream>>>(c->d_geo, N, d_smp, ns, c->blended, d_B);
+    HHG_LAUNCHED(c);
+  }
+  k_fit_coef<<<(unsigned)c->nt_local, ((15 * mq + 31) / 32) * 32, 0, c->stream>>>(
+      d_pinv, d_samples ? d_samples : d_B, ns, mq, d_scale, lv.d_coef);
+  HHG_LAUNCHED(c);
+  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(d_smp);
+  cudaFree(d_pinv);
+  if (d_B) cudaFree(d_B);
+  cudaFree(d_scale);
+  return make_coef10(c, lv, q, mq);
+}
+
+static hhg_status fit_args(Ctx* c, int q, hhg_fit_method method) {
+  if (!c) return HHG_ERR_INVALID;
+  if (c->poisoned) return HHG_ERR_CUDA;
+  if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context");
+  if (q < 0 || q > 4) return set_err(c, HHG_ERR_INVALID, "q must be in 0..4 (PAPER.md:530-534)");
+  if (method != HHG_FIT_LSQP && method != HHG_FIT_IPOLY) return set_err(c, HHG_ERR_INVALID, "method");
+  if (method == HHG_FIT_IPOLY && q != 2)
+    return set_err(c, HHG_ERR_INVALID, "IPOLY points are defined for q = 2 (PAPER.md:490-499)");
+  if (c->vc_graph) {  // a cached V-cycle graph holds the old coefficient buffers
+    cudaStreamSynchronize(c->stream);
+    cudaGraphExecDestroy(c->vc_graph);
+    c->vc_graph = nullptr;
+  }
+  return HHG_OK;
+}
+
 }  // namespace hhg
 
 using namespace hhg;
 
 extern "C" hhg_status hhg_fit_surrogates(hhg_ctx ctx, int q, hhg_fit_method method, int sampling_j) {
   Ctx* c = (Ctx*)ctx;
-  if (!c) return HHG_ERR_INVALID;
-  if (c->poisoned) return HHG_ERR_CUDA;
-  if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context");
-  if (q < 0 || q > 4) return set_err(c, HHG_ERR_INVALID, "q must be in 0..4 (PAPER.md:530-534)");
-  if (method != HHG_FIT_LSQP && method != HHG_FIT_IPOLY) return set_err(c, HHG_ERR_INVALID, "method");
-  if (c->vc_graph) {  // a cached V-cycle graph holds the old coefficient buffers
-    cudaStreamSynchronize(c->stream);
-    cudaGraphExecDestroy(c->vc_graph);
-    c->vc_graph = nullptr;
-  }
-  if (method == HHG_FIT_IPOLY && q != 2)
-    return set_err(c, HHG_ERR_INVALID, "IPOLY points are defined for q = 2 (PAPER.md:490-499)");
+  hhg_status st = fit_args(c, q, method);
+  if (st != HHG_OK) return st;
   const int mq = n_coeffs(q);
-  std::vector<int> el, em, en;
-  exponents(q, el, em, en);
-  // q <= 2: the march kernels read coefficients zero-padded to the q = 2 layout
-  // (the degree-major exponent list of q is a prefix of that of q = 2).
-  auto make10 = [&](Level& lv) -> hhg_status {
-    if (lv.d_coef10) cudaFree(lv.d_coef10);
-    lv.d_coef10 = nullptr;
-    if (lv.d_cC) cudaFree(lv.d_cC);  // derived from d_coef10 on first use (ops.cu)
-    lv.d_cC = nullptr;
-    if (q > 2) return HHG_OK;
-    HHG_CK(c, cudaMalloc(&lv.d_coef10, c->nt_local * 150 * sizeof(double)));
-    HHG_CK(c, cudaMemsetAsync(lv.d_coef10, 0, c->nt_local * 150 * sizeof(double), c->stream));
-    HHG_CK(c, cudaMemcpy2DAsync(lv.d_coef10, 10 * sizeof(double), lv.d_coef, mq * sizeof(double),
-                                mq * sizeof(double), c->nt_local * 15, cudaMemcpyDeviceToDevice, c->stream));
-    return HHG_OK;
-  };
+  bool bad = false;
   for (int L = 2; L <= c->L_max; ++L) {
     Level& lv = c->levels[L];
-    const int N = lv.N;
-    if (lv.d_coef) cudaFree(lv.d_coef);
-    lv.d_coef = nullptr;
-    HHG_CK(c, cudaMalloc(&lv.d_coef, c->nt_local * 15 * mq * sizeof(double)));
-    lv.q = q;
-    lv.mq = mq;
-    if (L == 2) {
-      k_exact_const<<<(unsigned)c->nt_local, 32, 0, c->stream>>>(c->d_geo, N, mq, c->blended, lv.d_coef);
+    if (L == 2) {  // l = 0: the exact stencil of the single interior node
+      if (lv.d_coef) cudaFree(lv.d_coef);
+      HHG_CK(c, cudaMalloc(&lv.d_coef, c->nt_local * 15 * mq * sizeof(double)));
+      lv.q = q;
+      lv.mq = mq;
+      k_exact_const<<<(unsigned)c->nt_local, 32, 0, c->stream>>>(c->d_geo, lv.N, mq, c->blended, lv.d_coef);
       HHG_LAUNCHED(c);
-      hhg_status st2 = make10(lv);
-      if (st2 != HHG_OK) return st2;
-      lv.fitted = true;
-      continue;
-    }
-    // sampling set
-    std::vector<int> smp;
-    if (method == HHG_FIT_IPOLY) {
-      int l = L - 2;
-      int a = (1 << (l + 2)) - 3, b = (1 << (l + 1)) - 1;
-      int pts[10][3] = {{1, 1, 1}, {1, 1, a}, {1, a, 1}, {a, 1, 1}, {1, 1, b},
-                        {1, b, 1}, {b, 1, 1}, {1, b, b}, {b, 1, b}, {b, b, 1}};
-      for (auto& p : pts) smp.insert(smp.end(), p, p + 3);
+      if ((st = make_coef10(c, lv, q, mq)) != HHG_OK) return st;
     } else {
-      int l = L - 2;
-      int m = std::min(l, std::max(1, sampling_j));
-      int Nm = 1 << (m + 2), sc = 1 << (l - m);
-      for (int k = 1; k < Nm; ++k)
-        for (int j = 1; j < Nm - k; ++j)
-          for (int i = 1; i < Nm - k - j; ++i) {
-            smp.push_back(i * sc);
-            smp.push_back(j * sc);
-            smp.push_back(k * sc);
-          }
+      if ((st = fit_level(c, lv, L, q, method, sampling_j, nullptr)) != HHG_OK) return st;
+      if ((st = fit_faces(c, lv, L, q, sampling_j)) != HHG_OK) return st;
     }
-    const int64_t ns = (int64_t)smp.size() / 3;
-    if (ns < mq) return set_err(c, HHG_ERR_FIT, "fewer sampling points than coefficients");
-    std::vector<double> A(ns * mq);
-    for (int64_t s = 0; s < ns; ++s)
-      for (int cc = 0; cc < mq; ++cc)
-        A[s * mq + cc] = std::pow((double)smp[3 * s] / N, el[cc]) *
-                         std::pow((double)smp[3 * s + 1] / N, em[cc]) *
-                         std::pow((double)smp[3 * s + 2] / N, en[cc]);
-    std::vector<double> pinv;
-    if (!pinv_qr(A, ns, mq, pinv))
-      return set_err(c, HHG_ERR_FIT, "rank-deficient sampling matrix at level " + std::to_string(L));
-    // index-unit scaling: x = i/N => a_lmn / N^(l+m+n) (exact powers of two)
-    std::vector<double> scale(mq);
-    for (int cc = 0; cc < mq; ++cc) scale[cc] = std::ldexp(1.0, -L * (el[cc] + em[cc] + en[cc]));
-    int* d_smp;
-    double *d_pinv, *d_B, *d_scale;
-    HHG_CK(c, cudaMalloc(&d_smp, smp.size() * sizeof(int)));
-    HHG_CK(c, cudaMalloc(&d_pinv, pinv.size() * sizeof(double)));
-    HHG_CK(c, cudaMalloc(&d_B, c->nt_local * ns * 15 * sizeof(double)));
-    HHG_CK(c, cudaMalloc(&d_scale, mq * sizeof(double)));
-    HHG_CK(c, cudaMemcpyAsync(d_smp, smp.data(), smp.size() * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-    HHG_CK(c, cudaMemcpyAsync(d_pinv, pinv.data(), pinv.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    HHG_CK(c, cudaMemcpyAsync(d_scale, scale.data(), mq * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    dim3 g1((unsigned)((ns + 127) / 128), (unsigned)c->nt_local);
-    k_sample_stencils<<<g1, 128, 0, c->stream>>>(c->d_geo, N, d_smp, ns, c->blended, d_B);
-    HHG_LAUNCHED(c);
-    k_fit_coef<<<(unsigned)c->nt_local, ((15 * mq + 31) / 32) * 32, 0, c->stream>>>(d_pinv, d_B, ns, mq, d_scale,
-                                                                               lv.d_coef);
-    HHG_LAUNCHED(c);
-    HHG_CK(c, cudaStreamSynchronize(c->stream));
-    cudaFree(d_smp);
-    cudaFree(d_pinv);
-    cudaFree(d_B);
-    cudaFree(d_scale);
-    hhg_status st2 = make10(lv);
-    if (st2 != HHG_OK) return st2;
-    if ((st2 = fit_faces(c, lv, L, q, sampling_j)) != HHG_OK) return st2;
+    if ((st = check_centre(c, lv)) != HHG_OK) return st;
+    bad = bad || lv.centre_bad || lv.fcentre_bad;
     lv.fitted = true;
   }
   HHG_CK(c, cudaStreamSynchronize(c->stream));
+  if (bad)
+    return set_err(c, HHG_ERR_NUMERIC,
+                   "non-positive surrogate centre weight: the fit is installed (apply/residual work), "
+                   "the GS smoother and V-cycle refuse it");
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_sample_nodes(hhg_ctx ctx, int L, hhg_fit_method method, int sampling_j, int32_t* ijk,
+                                       int64_t* n) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c || !n || L < 3 || L > c->L_max) return c ? set_err(c, HHG_ERR_INVALID, "L must be in 3..L_max") : HHG_ERR_INVALID;
+  if (method != HHG_FIT_LSQP && method != HHG_FIT_IPOLY) return set_err(c, HHG_ERR_INVALID, "method");
+  const std::vector<int> smp = sample_set(L, method, sampling_j);
+  *n = (int64_t)smp.size() / 3;
+  if (ijk) std::copy(smp.begin(), smp.end(), ijk);
+  return HHG_OK;
+}
+
+extern "C" hhg_status hhg_fit_from_samples(hhg_ctx ctx, int L, int q, hhg_fit_method method, int sampling_j,
+                                           const double* samples) {
+  Ctx* c = (Ctx*)ctx;
+  hhg_status st = fit_args(c, q, method);
+  if (st != HHG_OK) return st;
+  if (L < 3 || L > c->L_max || !samples) return set_err(c, HHG_ERR_INVALID, "L must be in 3..L_max, samples non-NULL");
+  const int64_t ns = (int64_t)sample_set(L, method, sampling_j).size() / 3;
+  const size_t bytes = (size_t)c->nt_local * ns * 15 * sizeof(double);
+  cudaPointerAttributes pa;
+  const bool dev = cudaPointerGetAttributes(&pa, samples) == cudaSuccess &&
+                   (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+  cudaGetLastError();
+  double* d_s = nullptr;
+  if (!dev) {
+    HHG_CK(c, cudaMalloc(&d_s, std::max<size_t>(bytes, 8)));
+    HHG_CK(c, cudaMemcpyAsync(d_s, samples, bytes, cudaMemcpyHostToDevice, c->stream));
+  }
+  Level& lv = c->levels[L];
+  st = fit_level(c, lv, L, q, method, sampling_j, dev ? samples : d_s);
+  if (d_s) cudaFree(d_s);
+  if (st != HHG_OK) return st;
+  // planted samples define no face polynomials: SURROGATE_FACES is unavailable on this level
+  if (lv.d_fcoef) cudaFree(lv.d_fcoef);
+  lv.d_fcoef = nullptr;
+  if ((st = check_centre(c, lv)) != HHG_OK) return st;
+  lv.fitted = true;
+  if (lv.centre_bad) return set_err(c, HHG_ERR_NUMERIC, "non-positive surrogate centre weight (installed; GS refuses it)");
   return HHG_OK;
 }

@@ -5,6 +5,8 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <map>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -112,7 +114,6 @@ struct Band {
 constexpr int kMarchThreads = 256;
 // opt-in dynamic shared memory limit of the march kernels (227 KB per block on sm_100, minus static)
 constexpr int kMaxDynSmem = 227 * 1024 - 1024;
-constexpr int kNarrowThreads = 128;
 constexpr int kRing = 16;  // plane slots (power of 2); >= 11 planes in flight ahead of use
 
 // Structured lower-primitive rows of one non-Dirichlet macro face (faces.cu).
@@ -162,16 +163,14 @@ struct Level {
   double* d_ew_lo = nullptr;       // [n_local] element-wise FEM: sums for the next band's first diagonal
   double* d_ew_hi = nullptr;       // [n_local] ... for the previous band's last diagonal
   bool fitted = false;
-  // column-march bands (<= kMarchThreads columns) and narrow bands (<= kNarrowThreads)
+  bool centre_bad = false;         // a surrogate centre weight <= 0 at some interior node (GS refuses: HHG_ERR_NUMERIC)
+  bool fcentre_bad = false;        // ... of a fitted face surrogate (SURROGATE_FACES GS refuses)
+  // column-march bands (<= kMarchThreads columns)
   std::vector<Band> bands;
   Band* d_bands = nullptr;
   int slot_len = 0;
-  std::vector<Band> bands_s;
-  Band* d_bands_s = nullptr;
   std::vector<Band> bands_fem;  // element-wise FEM: <= kMarchThreads anchor columns per band
   Band* d_bands_fem = nullptr;
-  int slot_len_s = 0;
-  int* d_gs_flags_s = nullptr;
   // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order
   int64_t n_flp = 0, n_frows = 0;
   int fcol[4] = {0, 0, 0, 0};      // colour offsets of q ((s+2t) mod 3 = 0,1,2)
@@ -218,10 +217,6 @@ struct Level {
   int* d_gs_flags = nullptr;   // [nt_local][n_bands][4] sweep epoch of completed colour passes
   int* d_gs_counter = nullptr; // [1]
   int gs_epoch = 0;
-  // static item schedule of the persistent kernels (pmarch.cuh), built on first use
-  int sched_grid = 0;
-  int* d_sched = nullptr;      // item ids, concatenated per CTA
-  int* d_sched_off = nullptr;  // [sched_grid + 1]
 };
 
 struct Ctx {
@@ -259,6 +254,9 @@ struct Ctx {
   double* d_geo = nullptr;            // [nt_local][4][4]: x,y,z,r per local vertex
   std::vector<Level> levels;          // index L
   int64_t launches = 0;
+  // per-context launch caches (a context is bound to one device)
+  std::set<const void*> smem_attr_done;                    // kernels with the >48 KB smem attribute set
+  std::map<std::pair<const void*, size_t>, int> grid_cache;  // co-resident grid per (kernel, smem)
   // host-vector staging
   double* d_stage[4] = {nullptr, nullptr, nullptr, nullptr};
   int64_t stage_n = 0;
@@ -272,6 +270,7 @@ struct Ctx {
   double* d_cg = nullptr;             // CG work: r p Ap at the coarse level (3 vectors)
   int64_t cg_n = 0;
   double* d_scal = nullptr;           // device scalars
+  int* d_flag = nullptr;              // device flag word (fit-time centre-weight check)
   // profiling (hhg_profile)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;
@@ -328,6 +327,7 @@ void exponents(int q, std::vector<int>& l, std::vector<int>& m, std::vector<int>
 // Distributed-memory support (dist.cu)
 hhg_status dist_init_transport(Ctx* c, const void* nccl_unique_id);
 void dist_destroy(Ctx* c);
+hhg_status ctx_sync(Ctx* c);
 hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& send_bytes, const void* send,
                                const std::vector<int64_t>& recv_bytes, void* recv, bool device);
 hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_slot,
@@ -345,6 +345,7 @@ hhg_status face_gather(Ctx* c, Level& lv, const double* local, double* glob, int
 hhg_status face_sync(Ctx* c, Level& lv, double* u);
 hhg_status face_dot(Ctx* c, Level& lv, const double* a, const double* b, double* part, int nblocks);
 hhg_status face_sum_copies(Ctx* c, Level& lv, double* v);
+hhg_status face_centre_check(Ctx* c, Level& lv, int* d_flag);
 
 // Operator pieces shared by ops.cu and vcycle.cu
 hhg_status apply_dev(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* y);
@@ -352,6 +353,7 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
 hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out);
 hhg_status dot_dev(Ctx* c, Level& lv, const double* a, const double* b, double* d_out);
 hhg_status zero_dir_slots(Ctx* c, Level& lv, double* out);
+hhg_status check_centre_ok(Ctx* c, const Level& lv, int op);
 hhg_status lp_sum_copies(Ctx* c, Level& lv, double* v);
 hhg_status lp_sync_own_copies(Ctx* c, Level& lv, double* v);
 // canonical global vector <-> local layout (ops.cu): owned entries into dglob
@@ -359,6 +361,8 @@ hhg_status lp_sync_own_copies(Ctx* c, Level& lv, double* v);
 hhg_status gather_owned_dev(Ctx* c, Level& lv, const double* local, double* dglob);
 hhg_status scatter_global_dev(Ctx* c, Level& lv, const double* dglob, double* local);
 // replicated coarse solve (coarse.cu)
+constexpr int64_t kCoarseMaxUnknowns = 1ll << 22;
+bool coarse_replicable(const Level& lv);
 hhg_status coarse_build(Ctx* c, Level& lv);
 hhg_status coarse_solve(Ctx* c, Level& lv, int iters, double* x, const double* b);
 hhg_status dist_allreduce_vec(Ctx* c, double* d_vec, int64_t n);

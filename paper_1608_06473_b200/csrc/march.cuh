@@ -66,6 +66,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Upper bound of a cross-CTA wait (polls of >= 32 ns: > 1 s) before it traps.
+constexpr long long kSpinLimit = 1ll << 25;
+
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -315,50 +318,12 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // thread visits its colour-c nodes k = delta + 4s (one per step of 4 planes).
 // The column coefficients (A, B) are computed by the caller once per band.
 // ---------------------------------------------------------------------------
-struct NoGate {
-  __device__ void wait(int) const {}
-  __device__ void publish(int) const {}
-};
 
-// Gate/publisher of the progress-gated GS (k_gs_items_p): before warp 0 issues
-// planes <= `to` of pass c, the two neighbour bands must have finished pass
-// c-1 up to plane to+1; after each refill barrier the band publishes how many
-// planes of pass c are done.
-struct ProgGate {
-  int* mine;            // own progress word
-  const int* left;      // neighbour words (nullptr: no neighbour)
-  const int* right;
-  int base;             // epoch * 8192
-  int colour;
-  __device__ void wait(int to) const {
-    if (colour == 0) return;
-    if (threadIdx.x == 0) {
-      const int want = base + (colour - 1) * 1024 + to + 2;
-      for (;;) {
-        int v = 0x7fffffff;
-        if (left) v = min(v, *(const volatile int*)left);
-        if (right) v = min(v, *(const volatile int*)right);
-        if (v >= want) break;
-        __nanosleep(64);
-      }
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    }
-    __syncwarp();
-    asm volatile("fence.proxy.async.global;" ::: "memory");
-  }
-  // called by all threads right after a __syncthreads
-  // (by the last warp: the release fence must not delay warp 0, the TMA issuer)
-  __device__ void publish(int done) const {
-    if (threadIdx.x == blockDim.x - 32)
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(mine), "r"(base + done) : "memory");
-  }
-};
-
-template <int OP, int RING = kRing, class Gate = NoGate>
+template <int OP, int RING = kRing>
 __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len, int N, const Band& b, const Column& q,
                                                const double (&A)[15], const double (&B)[15], int colour,
                                                double* __restrict__ ub, const double* __restrict__ fb,
-                                               double* __restrict__ wb, const Gate& gate = Gate()) {
+                                               double* __restrict__ wb) {
   if (threadIdx.x == 0) {
     for (int s = 0; s < RING; ++s) mbar_init(&sm.bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -368,7 +333,6 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
   const int last_plane = b.kmax + 1;
   int next_issue = min(RING, last_plane + 1);
-  if (threadIdx.x < 32) gate.wait(next_issue - 1);
   issue_planes<RING>(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
   const int clo = b.c_lo;
   auto sptr = [&](int p) -> const double* {
@@ -433,9 +397,7 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
     // RING = 24 the planes of the step after the next refill are already in flight).
     if (s % 3 == 2 || s == nsteps - 1) {
       __syncthreads();
-      gate.publish(colour * 1024 + min(4 * s + 4, last_plane + 1));
       const int to = min(4 * s + 2 + RING, last_plane);
-      if (to >= next_issue && threadIdx.x < 32) gate.wait(to);
       issue_planes<RING>(ub, sm.po, next_issue, to, b, sm.ring, slot_len, sm.bars);
       next_issue = max(next_issue, to + 1);
     }
@@ -446,12 +408,12 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
 // slots of 4 planes whose bulk copies complete on one barrier (arrival count
 // 4: one arrive.expect_tx per plane, plain arrives past the last plane), so a
 // thread waits once per step (4 planes) instead of four times.
-template <int OP, int RING, class Gate = NoGate>
+template <int OP, int RING>
 __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_len, int N, const Band& b,
                                                  const Column& q, const double (&A)[15], const double (&B)[15],
                                                  int colour, double* __restrict__ ub, const double* __restrict__ fb,
                                                  double* __restrict__ wb, const double* __restrict__ Cw,
-                                                 const Gate& gate = Gate(), bool init_bars = true) {
+                                                 bool init_bars = true) {
   constexpr int NQ = RING / 4;
 #ifdef HHG_GS_PROF
   long long _tp0 = clock64();
@@ -470,7 +432,6 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
   // warp 0: issue quads [q0, q1] (lane = plane within the group)
   auto issue_quads = [&](int q0, int q1) {
     if (threadIdx.x < 32 && q1 >= q0) {
-      gate.wait(min(4 * q1 + 3, last_plane));
       for (int p = 4 * q0 + (int)threadIdx.x; p <= 4 * q1 + 3; p += 32) {
         uint64_t* bar = &sm.bars[(p >> 2) % NQ];
         if (p <= last_plane) {
@@ -555,7 +516,6 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
       GPROF_T0
       __syncthreads();
       GPROF_ADD(7)
-      gate.publish(colour * 1024 + min(4 * s + 4, last_plane + 1));
       const int to = min(s - 1 + NQ, last_quad);
       {
         GPROF_T0
@@ -620,20 +580,13 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // running yet; every other running item's neighbours run too => no deadlock
 // while the grid has more CTAs than a macro has bands.
 // ---------------------------------------------------------------------------
-// ST (static schedule, default): CTA x takes items x, x + grid, x + 2 grid, ...
-// of the launch's macro chunk [T0, T0 + ntl), so the item -- and the macro's 15
-// C_w in the constant bank (g_cC, uploaded per chunk) -- are uniform: they sit
-// in uniform registers as DFMA operands.  Deadlock-free with every CTA
-// resident: pass c of item j waits only on items j +- 1 at pass c-1, so the
-// items of a wave finish their first passes without the next wave and at
-// least grid - 3 CTAs of a wave complete and move on.  !ST: items from an
-// atomic counter, C_w through shared memory.
-template <int OP, int NT, int RING, bool ST>
+// Items come from an atomic counter; C_w through shared memory.
+template <int OP, int NT, int RING>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
-               const double* __restrict__ f, int64_t ntl, int T0, int* __restrict__ counter,
-               int* __restrict__ flags, int epoch) {
+               const double* __restrict__ f, int64_t ntl, int* __restrict__ counter, int* __restrict__ flags,
+               int epoch) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem<RING> sm(smem, slot_len);
   __shared__ int s_item;
@@ -641,19 +594,15 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 #ifdef HHG_GS_PROF
   if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)(-clock64()));
 #endif
-  for (int64_t it = blockIdx.x;; it += gridDim.x) {
-    int64_t item = it;
-    if (!ST) {
-      if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
-      __syncthreads();
-      item = s_item;
-      __syncthreads();
-    }
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    __syncthreads();
     if (item >= total) break;
-    const int Tl = (int)(item / n_bands);
-    const int64_t T = T0 + Tl;
-    const int band = (int)(item - (int64_t)Tl * n_bands);
-    const double* const Cw = ST ? g_cC + Tl * 15 : sm.Cw;
+    const int64_t T = item / n_bands;
+    const int band = (int)(item - T * n_bands);
+    const double* const Cw = sm.Cw;
     const Band b = bands[band];
     Column q;
     double A[15], B[15];
@@ -670,7 +619,12 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         for (int bb = band - 1; bb <= band + 1; bb += 2) {
           if (bb < 0 || bb >= n_bands) continue;
           const int* fl = flags + ((T * n_bands + bb) * 4 + colour - 1);
-          while (ld_acquire_gpu(fl) != epoch) __nanosleep(32);
+          // bounded wait: a protocol fault traps (sticky launch error,
+          // HHG_ERR_CUDA) instead of hanging the device
+          for (long long spin = 0; ld_acquire_gpu(fl) != epoch; ++spin) {
+            if (spin > kSpinLimit) __trap();
+            __nanosleep(32);
+          }
         }
       }
       __syncthreads();
@@ -682,7 +636,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         GPROF_T0
         if (kQuad)
           gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
-                                     u + T * S + q.c, Cw, NoGate(), false);
+                                     u + T * S + q.c, Cw, false);
         else
           gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
         {
@@ -701,47 +655,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
 #ifdef HHG_GS_PROF
   if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)clock64());
 #endif
-}
-
-// Same items and colour passes, but with PLANE-level dependencies: pass c of
-// band b may load plane p as soon as bands b-1, b+1 have finished pass c-1 up
-// to plane p+1 (each band publishes its progress at every ring refill), so a
-// pass overlaps the tail of its neighbours' previous pass instead of waiting
-// for their completion.  prog[T][b] = epoch * 8192 + pass * 1024 + planes done.
-template <int OP, int NT, int RING>
-__global__ void __launch_bounds__(NT, 512 / NT)
-    k_gs_items_p(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
-                 const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
-                 const double* __restrict__ f, int64_t ntl, int* __restrict__ counter, int* __restrict__ prog,
-                 int epoch) {
-  extern __shared__ __align__(16) double smem[];
-  MarchSmem<RING> sm(smem, slot_len);
-  __shared__ int s_item;
-  const int64_t total = ntl * n_bands;
-  for (;;) {
-    if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
-    __syncthreads();
-    const int64_t item = s_item;
-    __syncthreads();
-    if (item >= total) break;
-    const int64_t T = item / n_bands;
-    const int band = (int)(item - T * n_bands);
-    const Band b = bands[band];
-    Column q;
-    double A[15], B[15];
-    band_setup<OP, RING>(sm, N, b, T, coef10, cons, q, A, B);
-    int* row = prog + T * n_bands;
-    ProgGate gate{row + band, band > 0 ? row + band - 1 : nullptr, band + 1 < n_bands ? row + band + 1 : nullptr,
-                  epoch * 8192, 0};
-    for (int colour = 0; colour < 4; ++colour) {
-      gate.colour = colour;
-      if (colour > 0 && threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
-      gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c,
-                               gate);
-      __syncthreads();
-      gate.publish((colour + 1) * 1024);
-    }
-  }
 }
 
 }  // namespace hhg

@@ -12,12 +12,7 @@
 #include "hhg_internal.h"
 #include "vol_kernels.cuh"
 #include "march.cuh"
-#include "pmarch.cuh"
-#include "pair.cuh"
-#include "gsq.cuh"
-#include "gswave.cuh"
 #include "gslex.cuh"
-#include "femmarch.cuh"
 #include "femew.cuh"
 
 namespace hhg {
@@ -227,11 +222,22 @@ static hhg_status stage(Ctx* c, int slot, const void* p, int64_t n, bool copy_in
 static hhg_status unstage(Ctx* c, Staged& s, int64_t n) {
   if (!s.staged) return HHG_OK;
   HHG_CK(c, cudaMemcpyAsync((void*)s.host, s.dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
   return HHG_OK;
 }
 
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+// The GS update divides by the centre weight (eq. iteration-scheme,
+// PAPER.md:1306-1315): a level whose fitted surrogate has a non-positive
+// centre weight somewhere (hhg_fit_surrogates' check) cannot be smoothed.
+hhg_status check_centre_ok(Ctx* c, const Level& lv, int op) {
+  if ((op == HHG_OP_SURROGATE || op == HHG_OP_SURROGATE_FACES) && lv.centre_bad)
+    return set_err(c, HHG_ERR_NUMERIC, "non-positive surrogate centre weight on level " + std::to_string(lv.L));
+  if (op == HHG_OP_SURROGATE_FACES && lv.fcentre_bad)
+    return set_err(c, HHG_ERR_NUMERIC, "non-positive face-surrogate centre weight on level " + std::to_string(lv.L));
+  return HHG_OK;
+}
 
 static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
   if (!c) return HHG_ERR_INVALID;
@@ -239,20 +245,12 @@ static hhg_status check_call(Ctx* c, int L, int op, bool smoother) {
   if (c->host_only) return set_err(c, HHG_ERR_STATE, "plan-only context (hhg_set_host_transport host_only)");
   if (L < 2 || L > c->L_max) return set_err(c, HHG_ERR_INVALID, "L out of range");
   if (op < 0 || op > 3) return set_err(c, HHG_ERR_INVALID, "bad op");
-  if ((op == HHG_OP_SURROGATE || op == HHG_OP_SURROGATE_FACES) && !c->levels[L].fitted)
+  const Level& lv = c->levels[L];
+  if ((op == HHG_OP_SURROGATE || op == HHG_OP_SURROGATE_FACES) && !lv.fitted)
     return set_err(c, HHG_ERR_STATE, "hhg_fit_surrogates must be called before using the surrogate operator");
-  (void)smoother;
-  return HHG_OK;
-}
-
-// The volume pass of one operation (apply / residual / GS colour).
-static bool force_v1() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HHG_VOLUME_KERNEL");
-    v = (e && std::string(e) == "v1") ? 1 : 0;
-  }
-  return v == 1;
+  if (op == HHG_OP_SURROGATE_FACES && L >= 3 && lv.n_flp > 0 && !lv.d_fcoef)
+    return set_err(c, HHG_ERR_STATE, "no face surrogates on this level (fitted from planted samples)");
+  return smoother ? check_centre_ok(c, lv, op) : HHG_OK;
 }
 
 // Per-macro k^2 coefficients C_w (coefficient 9 of each weight polynomial),
@@ -265,17 +263,40 @@ static hhg_status ensure_cC(Ctx* c, Level& lv, int op) {
   return HHG_OK;
 }
 
+// Opt-in dynamic shared memory for a kernel, once per context (a context is
+// bound to one device; the attribute is per device).
+static hhg_status smem_attr(Ctx* c, const void* fn) {
+  if (c->smem_attr_done.count(fn)) return HHG_OK;
+  HHG_CK(c, cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
+  c->smem_attr_done.insert(fn);
+  return HHG_OK;
+}
+
+// Co-resident grid of a persistent kernel (SMs x resident CTAs per SM), per
+// context and (kernel, dynamic shared memory).
+static hhg_status resident_grid(Ctx* c, const void* fn, int threads, size_t smem, int& grid) {
+  auto key = std::make_pair(fn, smem);
+  auto it = c->grid_cache.find(key);
+  if (it != c->grid_cache.end()) {
+    grid = it->second;
+    return HHG_OK;
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  HHG_CK(c, cudaGetDevice(&dev));
+  HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem));
+  grid = sms * per_sm;
+  c->grid_cache[key] = grid;
+  return HHG_OK;
+}
+
 template <int OP, int MODE>
 static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
-  static bool attr = false;
-  if (!attr) {
-    HHG_CK(c, cudaFuncSetAttribute(k_vol_march<OP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    attr = true;
-  }
-  const int nb = (int)lv.bands.size();
-  hhg_status st = ensure_cC(c, lv, OP);
+  hhg_status st = smem_attr(c, (const void*)k_vol_march<OP, MODE>);
   if (st != HHG_OK) return st;
+  const int nb = (int)lv.bands.size();
+  if ((st = ensure_cC(c, lv, OP)) != HHG_OK) return st;
   ProfScope ps(c, 0);
   for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
     const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
@@ -289,116 +310,12 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
   return HHG_OK;
 }
 
-// Persistent apply/residual (pmarch.cuh).  HHG_APPLY_KERNEL=march selects the
-// one-CTA-per-(macro,band) kernel above; p1 / p2 the persistent kernel with 1 / 2
-// nodes per thread step (default p2).
-static int apply_kernel_choice() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HHG_APPLY_KERNEL");
-    v = 0;
-    if (e && std::string(e) == "pair8") v = 5;
-    if (e && std::string(e) == "p1") v = 1;
-  }
-  return v;
-}
-
-// Persistent-grid size and the per-level static item schedule (pmarch.cuh).
-static hhg_status ensure_schedule(Ctx* c, Level& lv, const void* kernel, int& grid) {
-  static int g = 0;
-  if (g == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    HHG_CK(c, cudaGetDevice(&dev));
-    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kPThreads,
-                                                            pmarch_smem_bytes(24, 520, 256, 64)));
-    g = sms * std::max(per_sm, 1);
-  }
-  grid = g;
-  if (lv.sched_grid == grid) return HHG_OK;
-  std::vector<int> items, off;
-  build_pmarch_schedule(lv.bands, c->nt_local, grid, items, off);
-  if (lv.d_sched) cudaFree(lv.d_sched);
-  if (lv.d_sched_off) cudaFree(lv.d_sched_off);
-  HHG_CK(c, cudaMalloc(&lv.d_sched, std::max<size_t>(items.size(), 1) * sizeof(int)));
-  HHG_CK(c, cudaMalloc(&lv.d_sched_off, off.size() * sizeof(int)));
-  if (!items.empty())
-    HHG_CK(c, cudaMemcpy(lv.d_sched, items.data(), items.size() * sizeof(int), cudaMemcpyHostToDevice));
-  HHG_CK(c, cudaMemcpy(lv.d_sched_off, off.data(), off.size() * sizeof(int), cudaMemcpyHostToDevice));
-  lv.sched_grid = grid;
-  return HHG_OK;
-}
-
-template <int OP, int MODE, int NPS, int R>
-static hhg_status launch_pmarch(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
-  const int nb = (int)lv.bands.size();
-  const size_t smem = pmarch_smem_bytes(R, lv.slot_len, lv.N, nb);
-  static bool attr = false;
-  if (!attr) {
-    HHG_CK(c, cudaFuncSetAttribute(k_vol_pmarch<OP, MODE, NPS, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   112 * 1024));
-    attr = true;
-  }
-  if (smem > 112 * 1024) return set_err(c, HHG_ERR_INVALID, "pmarch: band too wide for shared memory");
-  int grid = 0;
-  hhg_status st = ensure_schedule(c, lv, (const void*)k_vol_pmarch<OP, MODE, NPS, R>, grid);
-  if (st != HHG_OK) return st;
-  ProfScope ps(c, 0);
-  k_vol_pmarch<OP, MODE, NPS, R><<<(unsigned)grid, kPThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, lv.d_sched, lv.d_sched_off);
-  HHG_LAUNCHED(c);
-  return HHG_OK;
-}
-
-template <int OP, int MODE, int R>
-static hhg_status launch_pair(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
-  const int nb = (int)lv.bands.size();
-  const size_t smem = pair_smem_bytes(R, lv.slot_len, lv.N, nb);
-  static int grid = 0;
-  if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_vol_pair<OP, MODE, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   112 * 1024));
-    int dev = 0, sms = 0, per_sm = 0;
-    HHG_CK(c, cudaGetDevice(&dev));
-    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vol_pair<OP, MODE, R>, kQThreads,
-                                                            pair_smem_bytes(R, 520, 256, 64)));
-    grid = sms * std::max(per_sm, 1);
-  }
-  if (smem > 112 * 1024) return set_err(c, HHG_ERR_INVALID, "pair march: band too wide for shared memory");
-  hhg_status st = ensure_cC(c, lv, OP);
-  if (st != HHG_OK) return st;
-  ProfScope ps(c, 0);
-  for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
-    const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
-    if (OP == HHG_OP_SURROGATE)
-      HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
-                                        cudaMemcpyDeviceToDevice, c->stream));
-    k_vol_pair<OP, MODE, R><<<(unsigned)std::min<int64_t>(grid, nt * nb), kQThreads, smem, c->stream>>>(
-        lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, out, nt, (int)T0);
-    HHG_LAUNCHED(c);
-  }
-  return HHG_OK;
-}
-
-template <int OP, int MODE>
-static hhg_status launch_apply_vol(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
-  switch (apply_kernel_choice()) {
-    case 0: return launch_march<OP, MODE>(c, lv, u, f, out);
-    case 1: return launch_pmarch<OP, MODE, 1, 16>(c, lv, u, f, out);
-    case 5: return launch_pair<OP, MODE, 8>(c, lv, u, f, out);
-    default: return launch_march<OP, MODE>(c, lv, u, f, out);
-  }
-}
-
+// One GS colour pass over every band (the fallback of the persistent sweep).
 template <int OP>
 static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, const double* f) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
-  static bool attr = false;
-  if (!attr) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_march<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    attr = true;
-  }
+  hhg_status st = smem_attr(c, (const void*)k_gs_march<OP>);
+  if (st != HHG_OK) return st;
   const int nb = (int)lv.bands.size();
   ProfScope ps(c, 1);
   k_gs_march<OP><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
@@ -407,189 +324,57 @@ static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, cons
   return HHG_OK;
 }
 
-template <int OP, int NT, int RING>
-static hhg_status launch_gs_items_nt(Ctx* c, Level& lv, double* u, const double* f) {
-  const bool narrow = NT == kNarrowThreads;
-  const std::vector<Band>& bands = narrow ? lv.bands_s : lv.bands;
-  const Band* d_bands = narrow ? lv.d_bands_s : lv.d_bands;
-  int* flags = narrow ? lv.d_gs_flags_s : lv.d_gs_flags;
-  const int slot_len = narrow ? lv.slot_len_s : lv.slot_len;
-  const size_t smem = march_smem_bytes(slot_len, lv.N, RING);
-  // persistent grid: every CTA resident (the flag waits rely on it), sized for
-  // this level's ring
-  static std::map<size_t, int> grids;
-  int& grid = grids[smem];
-  if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_items<OP, NT, RING, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    int dev = 0, sms = 0, per_sm = 0;
-    HHG_CK(c, cudaGetDevice(&dev));
-    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_items<OP, NT, RING, true>, NT, smem));
-    grid = sms * std::max(per_sm, 1);
-  }
-  const int nb = (int)bands.size();
+// The whole volume GS (4 colours) as one persistent launch (march.cuh::k_gs_items).
+template <int OP, int RING>
+static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* f) {
+  const size_t smem = march_smem_bytes(lv.slot_len, lv.N, RING);
+  const void* fn = (const void*)k_gs_items<OP, kMarchThreads, RING>;
+  hhg_status st = smem_attr(c, fn);
+  if (st != HHG_OK) return st;
+  int grid = 0;
+  if ((st = resident_grid(c, fn, kMarchThreads, smem, grid)) != HHG_OK) return st;
+  const int nb = (int)lv.bands.size();
   // deadlock freedom needs every band of the partially handed-out macro
   // resident at once (an item waits on its neighbour bands): otherwise use the
   // colour-pass kernels (no cross-CTA waits)
   if (grid <= nb) return HHG_ERR_STATE;
-  static int gated = -1;  // HHG_GS_DEPS=gate -> plane-level progress gating (k_gs_items_p; measured slower)
-  if (gated < 0) {
-    const char* e = getenv("HHG_GS_DEPS");
-    gated = (e && std::string(e) == "gate") ? 1 : 0;
-  }
   // completion flags cleared per sweep (epoch 1): the launch is replayable from
   // a CUDA graph (hhg_vcycle)
-  HHG_CK(c, cudaMemsetAsync(flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
   lv.gs_epoch = 1;
   HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
   const int64_t items = c->nt_local * nb;
   ProfScope ps(c, 1);
-  if (gated) {
-    static bool attr = false;
-    if (!attr) {
-      HHG_CK(c, cudaFuncSetAttribute(k_gs_items_p<OP, NT, RING>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kMaxDynSmem));
-      attr = true;
-    }
-    k_gs_items_p<OP, NT, RING><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
-        lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter, flags,
-        lv.gs_epoch);
-  } else {
-    // default: items from an atomic counter, C_w in shared memory;
-    // HHG_GS_SCHED=static: round-robin items, C_w in uniform registers (measured
-    // slower: 3.74 vs 3.05 ms, the static mix of long and short bands per CTA)
-    static int dyn = -1;
-    if (dyn < 0) {
-      const char* e = getenv("HHG_GS_SCHED");
-      dyn = (e && std::string(e) == "static") ? 0 : 1;
-    }
-    if (dyn) {
-      k_gs_items<OP, NT, RING, false><<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
-          lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, 0, lv.d_gs_counter, flags,
-          lv.gs_epoch);
-      HHG_LAUNCHED(c);
-    } else {
-      hhg_status st = ensure_cC(c, lv, OP);
-      if (st != HHG_OK) return st;
-      // macro chunks of <= kCMax (the constant-bank C_w table); chunks run in order
-      for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
-        const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
-        if (OP == HHG_OP_SURROGATE)
-          HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
-                                            cudaMemcpyDeviceToDevice, c->stream));
-        k_gs_items<OP, NT, RING, true><<<(unsigned)std::min<int64_t>(grid, nt * nb), NT, smem, c->stream>>>(
-            lv.N, lv.S, d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, nt, (int)T0, lv.d_gs_counter, flags,
-            lv.gs_epoch);
-        HHG_LAUNCHED(c);
-      }
-    }
-  }
-  return HHG_OK;
-}
-
-template <int OP>
-static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f) {
-  static int nt = -1;
-  if (nt < 0) {
-    const char* e = getenv("HHG_GS_CTA");
-    nt = (e && atoi(e) == 128) ? 128 : 256;
-  }
-  static int ring = -1;  // HHG_GS_RING=16 -> the apply kernels' ring depth
-  if (ring < 0) {
-    const char* e = getenv("HHG_GS_RING");
-    ring = (e && atoi(e) == 16) ? 16 : 24;
-  }
-  if (nt == 128 && !lv.bands_s.empty()) return launch_gs_items_nt<OP, kNarrowThreads, 24>(c, lv, u, f);
-  // 24-plane ring only while two CTAs fit an SM (N = 256: 768-double slots -> 16)
-  if (ring == 16 || march_smem_bytes(lv.slot_len, lv.N, 24) > 113 * 1024)
-    return launch_gs_items_nt<OP, kMarchThreads, 16>(c, lv, u, f);
-  return launch_gs_items_nt<OP, kMarchThreads, 24>(c, lv, u, f);
-}
-
-// Experimental single-pass wavefront GS (gswave.cuh, HHG_GS_KERNEL=wave).
-template <int OP>
-static hhg_status launch_gs_wave(Ctx* c, Level& lv, double* u, const double* f) {
-  const size_t smem = (size_t)kWRing * lv.slot_len * 8 + (kWRing + 4) * 8 + 16 * 8 + (size_t)(lv.N + 2) * 4;
-  static std::map<size_t, int> grids;
-  int& grid = grids[smem];
-  if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_wave<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    int dev = 0, sms = 0, per_sm = 0;
-    HHG_CK(c, cudaGetDevice(&dev));
-    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_wave<OP>, kWThreads, smem));
-    grid = sms * per_sm;
-  }
-  const int nb = (int)lv.bands.size();
-  // halo columns per band must fit the synchronisation warp (N <= 130), and
-  // every band of the last handed-out macro must be resident
-  if (lv.N > 130 || grid <= nb) return HHG_ERR_STATE;
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * sizeof(int), c->stream));
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
-  const int64_t items = c->nt_local * nb;
-  ProfScope ps(c, 1);
-  k_gs_wave<OP><<<(unsigned)std::min<int64_t>(grid, items), kWThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter,
-      lv.d_gs_flags);
-  HHG_LAUNCHED(c);
-  return HHG_OK;
-}
-
-// Whole volume GS sweep as one continuously pipelined persistent launch (gsq.cuh).
-template <int OP>
-static hhg_status launch_gs_quad(Ctx* c, Level& lv, double* u, const double* f) {
-  const size_t smem = gsq_smem_bytes(lv.slot_len, lv.N);
-  static int grid = 0;
-  if (grid == 0) {
-    HHG_CK(c, cudaFuncSetAttribute(k_gs_quad<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-    int dev = 0, sms = 0, per_sm = 0;
-    HHG_CK(c, cudaGetDevice(&dev));
-    HHG_CK(c, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    HHG_CK(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_gs_quad<OP>, kGThreads,
-                                                            gsq_smem_bytes(520, 256)));
-    grid = sms * std::max(per_sm, 1);
-  }
-  if (smem > (size_t)kMaxDynSmem) return set_err(c, HHG_ERR_INVALID, "gs: band too wide for shared memory");
-  const int nb = (int)lv.bands.size();
-  if (lv.gs_epoch >= 200000) {  // progress words encode epoch * 8192: restart the epochs
-    HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
-    lv.gs_epoch = 0;
-  }
-  lv.gs_epoch += 1;
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
-  const int64_t items = c->nt_local * nb;
-  ProfScope ps(c, 1);
-  k_gs_quad<OP><<<(unsigned)std::min<int64_t>(grid, items), kGThreads, smem, c->stream>>>(
+  k_gs_items<OP, kMarchThreads, RING><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
       lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter,
       lv.d_gs_flags, lv.gs_epoch);
   HHG_LAUNCHED(c);
   return HHG_OK;
 }
 
+template <int OP>
+static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f) {
+  // 24-plane ring only while two CTAs fit an SM (N = 256: 768-double slots -> 16)
+  if (march_smem_bytes(lv.slot_len, lv.N, 24) > 113 * 1024) return launch_gs_items_r<OP, 16>(c, lv, u, f);
+  return launch_gs_items_r<OP, 24>(c, lv, u, f);
+}
+
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
                               const double* f, double* out) {
   if (op == HHG_OP_SURROGATE_FACES) op = HHG_OP_SURROGATE;  // volume rows: the surrogate
-  if (mode == kModeGS && !force_v1() && !lv.bands.empty()) {
-    if (op == HHG_OP_SURROGATE && lv.d_coef10) return launch_gs_march<HHG_OP_SURROGATE>(c, lv, colour, out, f);
-    if (op == HHG_OP_CONST_AFFINE) return launch_gs_march<HHG_OP_CONST_AFFINE>(c, lv, colour, out, f);
+  // column-march kernels: q <= 2 surrogate (s_w quadratic along a column) and the constant stencil
+  const bool march = !lv.bands.empty() && ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
+  if (march && mode == kModeGS)
+    return op == HHG_OP_SURROGATE ? launch_gs_march<HHG_OP_SURROGATE>(c, lv, colour, out, f)
+                                  : launch_gs_march<HHG_OP_CONST_AFFINE>(c, lv, colour, out, f);
+  if (march) {
+    if (op == HHG_OP_SURROGATE)
+      return mode == kModeApply ? launch_march<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out)
+                                : launch_march<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out);
+    return mode == kModeApply ? launch_march<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
+                              : launch_march<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
   }
-  if (mode != kModeGS && !force_v1() && !lv.bands.empty()) {
-    if (op == HHG_OP_SURROGATE && lv.d_coef10) {
-      return mode == kModeApply ? launch_apply_vol<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out)
-                                : launch_apply_vol<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out);
-    }
-    if (op == HHG_OP_CONST_AFFINE) {
-      return mode == kModeApply ? launch_apply_vol<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
-                                : launch_apply_vol<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
-    }
-  }
-  static int fem_kernel = -1;  // HHG_FEM_KERNEL=node -> node-wise k_vol_fem (24 tets per node)
-  if (fem_kernel < 0) {
-    const char* e = getenv("HHG_FEM_KERNEL");
-    fem_kernel = (e && std::string(e) == "node") ? 1 : 0;
-  }
-  if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !force_v1() && !lv.bands.empty() && fem_kernel == 0) {
+  if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !lv.bands.empty()) {
     // plane range per band (the first band's also holds diagonal 0)
     int need = 0;
     for (const Band& bb : lv.bands_fem) need = std::max(need, bb.ncols + (bb.d0 == 2 ? bb.c_lo : 0));
@@ -597,12 +382,9 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
     const size_t smem = ew_smem_bytes(slot, lv.N);
     if (need + 1 > kFPosPerThread * kMarchThreads || smem > (size_t)kMaxDynSmem)
       return set_err(c, HHG_ERR_INVALID, "fem: band ring wider than the element-wise kernel");
-    static bool attr = false;
-    if (!attr) {
-      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem_ew<kModeApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem_ew<kModeResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-      attr = true;
-    }
+    hhg_status st = smem_attr(c, (const void*)k_vol_fem_ew<kModeApply>);
+    if (st == HHG_OK) st = smem_attr(c, (const void*)k_vol_fem_ew<kModeResid>);
+    if (st != HHG_OK) return st;
     if (!lv.d_ew_lo) {
       HHG_CK(c, cudaMalloc(&lv.d_ew_lo, lv.n_local * sizeof(double)));
       HHG_CK(c, cudaMalloc(&lv.d_ew_hi, lv.n_local * sizeof(double)));
@@ -629,27 +411,8 @@ static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, c
     }
     return HHG_OK;
   }
-  if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !force_v1() && !lv.bands.empty()) {
-    const size_t smem = fem_smem_bytes(lv.slot_len, lv.N);
-    if (lv.slot_len > kFPosPerThread * kMarchThreads)
-      return set_err(c, HHG_ERR_INVALID, "fem: band ring wider than the position pass");
-    static bool attr = false;
-    if (!attr) {
-      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeApply>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-      HHG_CK(c, cudaFuncSetAttribute(k_vol_fem<kModeResid>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem));
-      attr = true;
-    }
-    const int nb = (int)lv.bands.size();
-    ProfScope ps(c, 0);
-    if (mode == kModeApply)
-      k_vol_fem<kModeApply><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
-          lv.N, lv.S, lv.d_bands, nb, lv.slot_len, c->d_geo, c->blended, u, f, out);
-    else
-      k_vol_fem<kModeResid><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
-          lv.N, lv.S, lv.d_bands, nb, lv.slot_len, c->d_geo, c->blended, u, f, out);
-    HHG_LAUNCHED(c);
-    return HHG_OK;
-  }
+  // one thread per lattice node: q = 3, 4 (the weights are not quadratic along
+  // a column) and the level with no march band
   dim3 grid(nblk(lv.P, 128), (unsigned)c->nt_local);
   ProfScope ps(c, mode == kModeGS ? 1 : 0);
   k_vol_v1<<<grid, 128, 0, c->stream>>>(lv.N, lv.S, lv.P, c->d_geo, lv.d_coef, lv.mq, lv.d_cons, op,
@@ -730,7 +493,7 @@ hhg_status norm2_of(Ctx* c, Level& lv, const double* r, double* out) {
   if (st != HHG_OK) return st;
   if ((st = dot_dev(c, lv, r, r, c->d_red + 2 * kRedBlocks)) != HHG_OK) return st;
   HHG_CK(c, cudaMemcpyAsync(c->h_red, c->d_red + 2 * kRedBlocks, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
   *out = std::sqrt(c->h_red[0]);
   return HHG_OK;
 }
@@ -787,30 +550,19 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
     if (st != HHG_OK) return st;
     return dist_sync(c, lv, u);
   }
-  static int mode = -1;  // HHG_GS_KERNEL: passes -> 4 colour launches, quad -> k_gs_quad, default k_gs_items
-  if (mode < 0) {
-    const char* e = getenv("HHG_GS_KERNEL");
-    mode = (e && std::string(e) == "passes") ? 1 : (e && std::string(e) == "quad") ? 0
-           : (e && std::string(e) == "wave") ? 3 : 2;
-  }
-  const bool march_ok = !force_v1() && !lv.bands.empty() &&
-                        ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
-  if (march_ok && mode == 0) {
-    hhg_status st = op == HHG_OP_SURROGATE ? launch_gs_quad<HHG_OP_SURROGATE>(c, lv, u, f)
-                                           : launch_gs_quad<HHG_OP_CONST_AFFINE>(c, lv, u, f);
-    if (st != HHG_OK) return st;
-  } else if (march_ok && mode == 3 &&
-             (op == HHG_OP_SURROGATE ? launch_gs_wave<HHG_OP_SURROGATE>(c, lv, u, f)
-                                     : launch_gs_wave<HHG_OP_CONST_AFFINE>(c, lv, u, f)) == HHG_OK) {
-  } else if (march_ok && (mode == 2 || mode == 3) &&
-             (op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
-                                     : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f)) == HHG_OK) {
-  } else {
+  // HHG_GS_KERNEL (read per call, so tests can compare the variants):
+  // "passes" = 4 colour launches; default = the persistent sweep k_gs_items
+  const char* e = getenv("HHG_GS_KERNEL");
+  const int mode = (e && std::string(e) == "passes") ? 1 : 2;
+  const bool march_ok = !lv.bands.empty() && ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
+  hhg_status st = HHG_ERR_STATE;
+  if (march_ok && mode == 2)
+    st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
+                                : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
+  if (st != HHG_OK) {
     if (c->poisoned) return HHG_ERR_CUDA;
-    for (int col = 0; col < 4; ++col) {
-      hhg_status st = volume_pass(c, lv, op, kModeGS, col, u, f, u);
-      if (st != HHG_OK) return st;
-    }
+    for (int col = 0; col < 4; ++col)
+      if ((st = volume_pass(c, lv, op, kModeGS, col, u, f, u)) != HHG_OK) return st;
   }
   return dist_sync(c, lv, u);  // ghost volume values for the other ranks
 }
@@ -931,7 +683,7 @@ extern "C" hhg_status hhg_gather_global(hhg_ctx ctx, int L, const double* local,
   if ((st = gather_owned_dev(c, lv, sl.dev, dglob)) != HHG_OK) return st;
   if (host_glob) {
     HHG_CK(c, cudaMemcpyAsync(glob, dglob, lv.gi.n_total * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
     cudaFree(dglob);
   }
   return HHG_OK;
@@ -957,7 +709,7 @@ extern "C" hhg_status hhg_scatter_global(hhg_ctx ctx, int L, const double* glob,
   if ((st = scatter_global_dev(c, lv, dglob, sl.dev)) != HHG_OK) return st;
   if ((st = unstage(c, sl, lv.n_local)) != HHG_OK) return st;
   if (tmp) {
-    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
     cudaFree(tmp);
   }
   return HHG_OK;
@@ -995,7 +747,7 @@ extern "C" hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t m
   HHG_LAUNCHED(c);
   if (so.staged) {
     HHG_CK(c, cudaMemcpyAsync(out, so.dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
   }
   return HHG_OK;
 }
@@ -1010,7 +762,7 @@ extern "C" hhg_status hhg_profile(hhg_ctx ctx, int enable) {
 extern "C" hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, int64_t* launches) {
   Ctx* c = (Ctx*)ctx;
   if (!c || kind < 0 || kind > 3) return HHG_ERR_INVALID;
-  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
   double tot = 0.0;
   for (auto& p : c->ev_rec[kind]) {
     float ms = 0.f;

@@ -240,7 +240,6 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   };
   if (!make_bands(kMarchThreads, lv.bands, lv.slot_len))
     return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA");
-  if (!make_bands(kNarrowThreads, lv.bands_s, lv.slot_len_s)) lv.bands_s.clear();  // N > 129: not used
   // element-wise FEM bands: <= kMarchThreads ANCHOR columns (every column of a
   // diagonal, d+1; the first band also anchors diagonal 1's 2 columns)
   lv.bands_fem.clear();
@@ -565,15 +564,11 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if ((st = up(lv.d_dir_slot, dslot)) != HHG_OK) return st;
   if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
   if ((st = up(lv.d_bands, lv.bands)) != HHG_OK) return st;
-  if ((st = up(lv.d_bands_s, lv.bands_s)) != HHG_OK) return st;
   if ((st = up(lv.d_bands_fem, lv.bands_fem)) != HHG_OK) return st;
   {
     const size_t nfl = (size_t)c->nt_local * std::max<size_t>(lv.bands.size(), 1) * 4;
     HHG_CK(c, cudaMalloc(&lv.d_gs_flags, nfl * sizeof(int)));
     HHG_CK(c, cudaMemset(lv.d_gs_flags, 0, nfl * sizeof(int)));
-    const size_t nfs = (size_t)c->nt_local * std::max<size_t>(lv.bands_s.size(), 1) * 4;
-    HHG_CK(c, cudaMalloc(&lv.d_gs_flags_s, nfs * sizeof(int)));
-    HHG_CK(c, cudaMemset(lv.d_gs_flags_s, 0, nfs * sizeof(int)));
     HHG_CK(c, cudaMalloc(&lv.d_gs_counter, sizeof(int)));
   }
   HHG_CK(c, cudaMalloc(&lv.d_val, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
@@ -599,7 +594,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_sched, lv.d_sched_off, lv.d_bands_s, lv.d_gs_flags_s, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red, lv.d_fne[0], lv.d_fne[1], lv.d_fne[2]};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red, lv.d_fne[0], lv.d_fne[1], lv.d_fne[2]};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();
@@ -875,6 +870,7 @@ extern "C" void hhg_destroy(hhg_ctx ctx) {
       if (p) cudaFree(p);
   if (c->d_cg) cudaFree(c->d_cg);
   if (c->d_scal) cudaFree(c->d_scal);
+  if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_own) cudaFree(c->d_own);
   if (c->vc_graph) cudaGraphExecDestroy(c->vc_graph);
   if (c->cap_stream) cudaStreamDestroy(c->cap_stream);

@@ -157,16 +157,13 @@ static hhg_status level_vec(Ctx* c, std::vector<double*>& v, int L) {
   return HHG_OK;
 }
 
-// Coarse solver selection: the replicated CSR solve (coarse.cu, default) or,
-// with HHG_COARSE=ops, CG through the library's operator calls (one apply, three
-// dot products and two updates per iteration) -- the same recurrence.
+// Coarse solver selection: the replicated CSR solve (coarse.cu, default) or CG
+// through the library's operator calls (one apply, three dot products and two
+// updates per iteration; the same recurrence) -- for coarse levels too large to
+// replicate (coarse_replicable), or forced with HHG_COARSE=ops.
 static bool coarse_ops() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("HHG_COARSE");
-    v = (e && std::string(e) == "ops") ? 1 : 0;
-  }
-  return v == 1;
+  const char* e = getenv("HHG_COARSE");  // read per call (tests compare both solvers)
+  return e && std::string(e) == "ops";
 }
 
 // x = A^-1 b by `iters` CG iterations from x = 0 on the exact FEM operator
@@ -239,7 +236,8 @@ static hhg_status vcycle_rec(Ctx* c, int L, int Lc, int nu1, int nu2, int cg_ite
                              double* u, const double* f) {
   hhg_status st;
   if (L == Lc)
-    return coarse_ops() ? coarse_cg_ops(c, L, cg_iters, u, f) : coarse_solve(c, c->levels[L], cg_iters, u, f);
+    return coarse_ops() || !coarse_replicable(c->levels[L]) ? coarse_cg_ops(c, L, cg_iters, u, f)
+                                                            : coarse_solve(c, c->levels[L], cg_iters, u, f);
   Level& lv = c->levels[L];
   for (int s = 0; s < nu1; ++s)
     if ((st = gs_sweep_dev(c, lv, op, u, f, lex)) != HHG_OK) return st;
@@ -302,13 +300,17 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: smoother op must be SURROGATE(_FACES) or CONST_AFFINE");
   if (c->host_only)
     return set_err(c, HHG_ERR_INVALID, "hhg_vcycle: needs device vectors (host_only context)");
-  for (int l = L_coarse; l <= L; ++l)
+  hhg_status st;
+  for (int l = L_coarse; l <= L; ++l) {
     if (!c->levels[l].fitted) return set_err(c, HHG_ERR_STATE, "hhg_vcycle: call hhg_fit_surrogates first");
-  hhg_status st = ensure_mg(c);
+    if (l > L_coarse && (st = check_centre_ok(c, c->levels[l], op)) != HHG_OK) return st;
+  }
+  st = ensure_mg(c);
   if (st != HHG_OK) return st;
   // the coarse matrix is assembled once per level (collective, synchronising:
   // never inside a graph capture)
-  if (!coarse_ops() && (st = coarse_build(c, c->levels[L_coarse])) != HHG_OK) return st;
+  if (!coarse_ops() && coarse_replicable(c->levels[L_coarse]) && (st = coarse_build(c, c->levels[L_coarse])) != HHG_OK)
+    return st;
   Level& lv = c->levels[L];
   const int64_t n = lv.n_local;
   // host vectors are staged
@@ -357,7 +359,7 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
   // Never with the host transport (host callbacks), while profiling, or with
   // the experimental GS variants.
   const char* ge = getenv("HHG_VCYCLE_GRAPH");
-  bool use_graph = ge && atoi(ge) == 1 && c->transport != 2 && !c->prof && !getenv("HHG_GS_DEPS") &&
+  bool use_graph = ge && atoi(ge) == 1 && c->transport != 2 && !c->prof && !getenv("HHG_COARSE") &&
                    !getenv("HHG_GS_KERNEL");
   // the graph is cached on the ctx and reused by later calls with the same
   // signature (levels, smoother, vectors)
@@ -422,7 +424,7 @@ static hhg_status vcycle_impl(Ctx* c, int L, int nu1, int nu2, int L_coarse, int
   if (hu) {
     HHG_CK(c, cudaMemcpyAsync(u, stage_u, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
   }
-  HHG_CK(c, cudaStreamSynchronize(c->stream));
+  { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
   if (stage_u) cudaFree(stage_u);
   if (stage_f) cudaFree(stage_f);
   return result;

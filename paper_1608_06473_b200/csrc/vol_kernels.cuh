@@ -41,7 +41,7 @@ __device__ inline void node_weights(int op, int N, int i, int j, int k, const do
   }
 }
 
-__global__ void k_vol_v1(int N, int64_t S, int64_t P, const double* __restrict__ geo,
+static __global__ void k_vol_v1(int N, int64_t S, int64_t P, const double* __restrict__ geo,
                          const double* __restrict__ coef, int mq, const double* __restrict__ cons,
                          int op, bool blended, int mode, int colour, const double* u,
                          const double* __restrict__ f, double* out) {

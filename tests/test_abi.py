@@ -20,7 +20,8 @@ def test_header_declares_the_survey_boundary():
     names = set(_declared())
     for n in ("hhg_setup_macro_mesh", "hhg_fit_surrogates", "hhg_apply", "hhg_residual",
               "hhg_gs_sweep", "hhg_vcycle", "hhg_gather_global", "hhg_scatter_global",
-              "hhg_vector_layout", "hhg_last_error", "hhg_destroy", "hhg_eval_stencils"):
+              "hhg_vector_layout", "hhg_last_error", "hhg_destroy", "hhg_eval_stencils", "hhg_fit_from_samples",
+              "hhg_sample_nodes"):
         assert n in names
 
 

@@ -9,13 +9,10 @@ one by one from its own definitions:
   assembly over the macros containing the node (PAPER.md:385-394, 632-636);
 * the on-the-fly FEM operator at volume nodes: the oracle's node stencils
   from the 24 incident fine tets (fem.volume_stencils, PAPER.md:385-394);
-* GS at volume nodes >= 5 lattice steps from their macro's boundary: the
-  colour-ordered update (R13/R14) replayed on the node's dependency
-  cone -- a colour-c node reads new values of its lower-colour neighbours,
-  which read theirs, at most 3 levels deep, and the deepest level reads its
-  neighbours 4 steps away -- all volume nodes with their old values (the
-  face class steps before the volume colours do not reach them), so the
-  replay is exact.
+* one GS sweep at sampled vertex, edge, face (near-edge and interior) and
+  volume nodes (interior and next to macro faces / edges): the class-step
+  order (R13/R14) replayed on the node's dependency cone with the
+  oracle's rows (surrogate at volume nodes, exact FEM at the others).
 
 Tolerance: |gpu - oracle| <= 1e-12 * sum_w |s_w u_w| per sampled node (the
 row's natural scale; north_star's 1e-12 relative).
@@ -141,44 +138,83 @@ def test_fullsize_lower_primitive_rows_sampled(t, nr, L):
         assert abs(out["r"][g] - (f[g] - ref)) <= TOL * (scale + abs(f[g])), g
 
 
+def _gs_replay(mesh, num, t, nr, L, u, f):
+    """new_value(g): node g after ONE hybrid GS sweep, replayed on its
+    dependency cone from the class-step definition (R13/R14,
+    oracle.Numbering.step_of): a node of step s is updated from the values
+    after step s-1 -- a neighbour of a lower step contributes its new value
+    (recursively), every other neighbour its old value; Dirichlet nodes are 0.
+    Rows: the surrogate at volume nodes (the oracle's fit of the node's macro),
+    the exact FEM row (node-wise assembly over every macro holding the node,
+    oracle.fem.fem_row) at face / edge / vertex nodes.
+    Returns (value, scale) with scale = (|f| + sum_w |s_w v_w|) / |s_mc|."""
+    N = 2 ** L
+    memo = {}
+
+    def row(g):
+        if g >= num.base_v:
+            T, ijk = num.locate(g)[0]
+            sw = S.eval_weights(coeffs(t, nr, L, T), ijk[None, :], N, 2)[0]
+            cols = num.gids(T, ijk[None, :] + DIRS)
+            return dict(zip((int(x) for x in cols), sw))
+        return fem.fem_row(mesh, num, g, blended=True, locs=num.locate(g))
+
+    def new_value(g):
+        if g in memo:
+            return memo[g]
+        sg = num.step_of(g)
+        acc, mag, diag = 0.0, 0.0, None
+        for c, w in row(g).items():
+            if c == g:
+                diag = w
+                continue
+            sc = num.step_of(c)
+            if sc < 0:
+                continue
+            v = new_value(c)[0] if sc < sg else u[c]
+            acc += w * v
+            mag += abs(w * v)
+        memo[g] = ((f[g] - acc) / diag, (abs(f[g]) + mag) / abs(diag))
+        return memo[g]
+    return new_value
+
+
 @pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7), (None, None, 8)])
 def test_fullsize_gs_sweep_sampled(t, nr, L):
+    """One hybrid GS sweep on the bench workload, sampled on EVERY node class
+    the smoother couples: vertex, edge and face nodes (face
+    nodes next to an edge -- the near-edge write path -- and in the face
+    interior), volume nodes next to a macro face or edge, and interior volume
+    nodes -- each replayed on its dependency cone by _gs_replay."""
     mesh, num, u, f, out = case(t, nr, L)
     N = 2 ** L
     rng = np.random.default_rng(4321 + L)
-    pts = sample_volume(rng, N, mesh.nt, 48, 5)
-    for T, i, j, k in pts:
-        a = coeffs(t, nr, L, T)
-        memo = {}
-
-        def colour(p):
-            return (p[0] + 2 * p[1] + 3 * p[2]) % 4
-
-        def new_value(p):
-            """(value, scale) of volume node p after the volume colour step
-            of its colour (the class steps before it do not touch volume
-            nodes); scale = (|f| + sum_w |s_w v_w|) / |s_mc|."""
-            if p in memo:
-                return memo[p]
-            c = colour(p)
-            ijk = np.array([p])
-            sw = S.eval_weights(a, ijk, N, 2)[0]
-            acc, mag = 0.0, 0.0
-            for w in range(15):
-                if w == MC:
-                    continue
-                q = (p[0] + DIRS[w][0], p[1] + DIRS[w][1], p[2] + DIRS[w][2])
-                v = new_value(q)[0] if colour(q) < c else u[int(num.gids(T, np.array([q]))[0])]
-                acc += sw[w] * v
-                mag += abs(sw[w] * v)
-            gp = int(num.gids(T, ijk)[0])
-            memo[p] = ((f[gp] - acc) / sw[MC], (abs(f[gp]) + mag) / abs(sw[MC]))
-            return memo[p]
-
-        p = (i, j, k)
-        ref, scale = new_value(p)
-        gI = int(num.gids(T, np.array([p]))[0])
-        assert abs(out["ug"][gI] - ref) <= TOL * scale, (T, p, out["ug"][gI], ref)
+    gids = []
+    # volume nodes: deep interior, within 1..3 steps of a macro face, and next to a macro edge
+    for T, i, j, k in sample_volume(rng, N, mesh.nt, 16, 5):
+        gids.append(int(num.gids(T, np.array([[i, j, k]]))[0]))
+    for x in range(16):
+        T = int(rng.integers(mesh.nt))
+        d = 1 + x % 3
+        ijk = [(d, 5 + x, 7), (9, d, 3 + x), (4 + x, 6, d), (d, d, 10 + x), (1, N - 3 - x, 1)][x % 5]
+        if sum(ijk) <= N - 1:
+            gids.append(int(num.gids(T, np.array([ijk]))[0]))
+    if t is not None:
+        unk_f = np.nonzero(num.unknown_mask[num.base_f:num.base_v])[0] + num.base_f
+        unk_e = np.nonzero(num.unknown_mask[num.base_e:num.base_f])[0] + num.base_e
+        unk_v = np.nonzero(num.unknown_mask[:num.base_e])[0]
+        # face nodes near an edge (s, t or N-s-t in {1, 2}) and in the interior of the face
+        near, far = [], []
+        for g in rng.choice(unk_f, 4000, replace=False):
+            s_, t_ = num._face_st(int(g - num.base_f) % num.nfi)
+            (near if min(s_, t_, N - s_ - t_) <= 2 else far).append(int(g))
+        gids += near[:10] + far[:4]
+        gids += [int(x) for x in rng.choice(unk_e, 6, replace=False)]
+        gids += [int(x) for x in rng.choice(unk_v, 3, replace=False)]
+    new_value = _gs_replay(mesh, num, t, nr, L, u, f)
+    for g in gids:
+        ref, scale = new_value(g)
+        assert abs(out["ug"][g] - ref) <= TOL * scale, (g, num.step_of(g), out["ug"][g], ref)
 
 
 @pytest.mark.parametrize("t,nr,L", [(1, 2, 6), (1, 2, 7), (None, None, 8)])

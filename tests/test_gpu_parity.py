@@ -19,6 +19,16 @@ def rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300)
 
 
+def elem_rel(a, b, scale):
+    """Element-wise max relative error: max_i |a_i - b_i| / scale_i, with scale_i
+    the magnitude of the terms summed into entry i (|L||u| + |f| for apply /
+    residual: the natural per-row scale of a rounding error)."""
+    a, b, scale = (np.asarray(x, dtype=np.float64) for x in (a, b, scale))
+    m = scale > 0
+    assert np.all(a[~m] == b[~m])
+    return float(np.max(np.abs(a[m] - b[m]) / scale[m])) if m.any() else 0.0
+
+
 MESHES = {
     "tet": lambda: synth.single_tet(),
     "shell60": lambda: synth.shell_mesh(0.55, 1.0, 0, 1),
@@ -66,8 +76,10 @@ def to_local(ctx, L, x):
 # ("tet", 7) is BASELINE config 2 at full size (129 nodes per edge, 36 bands of
 # the march kernels); the 480-macro configs at L = 6, 7 are checked on sampled
 # outputs in test_gpu_fullsize.py
+# ("shell480", 5): the 480-macro shell of the bench workload at L = 5 (2.66 M
+# nodes, 2 march bands per macro, curved non-Dirichlet faces) full-vector
 CASES = [("tet", 2), ("tet", 3), ("tet", 4), ("tet", 5), ("tet", 6), ("tet", 7), ("shell60", 3), ("shell60", 4),
-         ("shell120", 3), ("shell480", 3)]
+         ("shell120", 3), ("shell480", 3), ("shell480", 5)]
 
 
 @pytest.mark.parametrize("mesh_name,L", CASES)
@@ -110,10 +122,16 @@ def test_apply_residual_gs_match_oracle(mesh_name, L):
     du, df, dy, dr = to_local(ctx, L, u), to_local(ctx, L, f), ctx.zeros(L), ctx.zeros(L)
     ctx.apply(L, du, dy)
     y_ref = solvers.apply(Lt, num, u)
-    assert rel(ctx.gather_global(L, dy), y_ref) < TOL
+    y = ctx.gather_global(L, dy)
+    assert rel(y, y_ref) < TOL
+    m = solvers.mask(num)
+    absLu = m * (abs(Lt) @ np.abs(m * u))
+    assert elem_rel(y, y_ref, absLu) < TOL
     nrm = ctx.residual(L, du, df, dr, norm=True)
     r_ref = solvers.residual(Lt, num, u, f)
-    assert rel(ctx.gather_global(L, dr), r_ref) < TOL
+    r = ctx.gather_global(L, dr)
+    assert rel(r, r_ref) < TOL
+    assert elem_rel(r, r_ref, absLu + m * np.abs(f)) < TOL
     assert abs(nrm - np.linalg.norm(r_ref)) <= TOL * np.linalg.norm(r_ref)
     # copies of lower primitives are all written consistently
     y2 = ctx.zeros(L)
@@ -124,7 +142,14 @@ def test_apply_residual_gs_match_oracle(mesh_name, L):
     ug = du.clone()
     ctx.gs_sweep(L, ug, df, 2)
     u_ref = gs.sweep(u.copy(), f, 2)
-    assert rel(ctx.gather_global(L, ug), u_ref) < TOL
+    u2 = ctx.gather_global(L, ug)
+    assert rel(u2, u_ref) < TOL
+    # per node: (|f| + sum_{w != mc} |s_w u_w|) / |s_mc| at the final iterate
+    # (the scale of the last update's rounding; the first sweep's errors are
+    # damped by the second)
+    d = np.where(m > 0, np.abs(gs.diag), 1.0)
+    sc = m * (np.abs(f) + abs(gs.off) @ np.abs(u_ref)) / d
+    assert elem_rel(u2, u_ref, sc) < 10 * TOL
 
 
 @pytest.mark.parametrize("mesh_name,L", [("tet", 4), ("tet", 6), ("tet", 7), ("shell60", 3), ("flat_tet", 4)])
@@ -155,7 +180,7 @@ def test_host_pointer_inputs_match_device():
 
 
 def test_ipoly_and_other_degrees():
-    for q, method in ((1, "lsqp"), (3, "lsqp"), (2, "ipoly")):
+    for q, method in ((1, "lsqp"), (3, "lsqp"), (4, "lsqp"), (2, "ipoly")):
         mesh, num, Lt, A, cf = oracle_case("tet", 5, q, method)
         ctx = gpu_ctx("tet", 5, q, method)
         got = ctx.eval_stencils(5, 0)
@@ -204,7 +229,8 @@ def oracle_hierarchy(mesh_name, L):
     return solvers.Hierarchy(MESHES[mesh_name](), L, 2, 2)
 
 
-@pytest.mark.parametrize("mesh_name,L,cycles", [("tet", 4, 3), ("shell60", 4, 3), ("shell120", 3, 2)])
+@pytest.mark.parametrize("mesh_name,L,cycles", [("tet", 4, 3), ("shell60", 4, 3), ("shell120", 3, 2),
+                                               ("shell480", 5, 2)])
 def test_vcycle_history_matches_oracle(mesh_name, L, cycles):
     """V(3,3), coarse 50 CG at L=2, 4-colour GS on every level: residual
     histories agree to 1e-10 relative (north_star), iterates to 1e-10."""
@@ -330,3 +356,130 @@ def test_vcycle_graph_replay_matches_eager(mesh_name, L, monkeypatch):
     hist_g = ctx.vcycle(L, du2, df, n_cycles=3)
     assert np.array_equal(hist_g, hist_e), (hist_g, hist_e)
     assert np.array_equal(ctx.gather_global(L, du2), ue)
+
+
+def _planted(rng, q, N):
+    """15 random polynomials of degree <= q in index units (monomials
+    i^l j^m k^n, l+m+n <= q) with a dominant positive centre weight."""
+    ex = [(l, m, n) for d in range(q + 1) for l in range(d, -1, -1) for m in range(d - l, -1, -1)
+          for n in [d - l - m]]
+    c = rng.uniform(-1, 1, (15, len(ex))) / np.array([float(N) ** sum(e) for e in ex])
+    c[7, 0] = 50.0
+
+    def ev(ijk):
+        ijk = np.asarray(ijk, dtype=np.float64)
+        mono = np.stack([ijk[:, 0] ** l * ijk[:, 1] ** m * ijk[:, 2] ** n for l, m, n in ex], axis=1)
+        return mono @ c.T  # [n, 15]
+    return ev
+
+
+@pytest.mark.parametrize("mesh_name,L,q_plant,q_fit,method", [("tet", 5, 2, 2, "lsqp"), ("shell60", 4, 1, 2, "lsqp"),
+                                                              ("shell60", 5, 2, 2, "ipoly"), ("tet", 4, 3, 3, "lsqp")])
+def test_fit_reproduces_planted_polynomials(mesh_name, L, q_plant, q_fit, method):
+    """hhg_fit_from_samples (test export): a planted weight field that is a
+    polynomial of degree <= q is reproduced exactly at every interior node
+    (the least-squares fit of an exactly representable field is the field,
+    PAPER.md:501-534) -- pins the library's sampling set, basis, QR
+    pseudo-inverse and index-unit scaling independently of the FEM sampler."""
+    import paper_1608_06473_b200 as hhg
+    mesh = MESHES[mesh_name]()
+    N = 2 ** L
+    ctx = hhg.Ctx.from_mesh(mesh, L)
+    rng = np.random.default_rng(10 * L + q_plant)
+    smp = ctx.sample_nodes(L, method, 2)
+    ref_smp = S.ipoly_samples(L) if method == "ipoly" else S.lsqp_samples(L, 2)
+    assert {tuple(x) for x in smp} == {tuple(x) for x in ref_smp}
+    fields = [_planted(rng, q_plant, N) for _ in range(mesh.nt)]
+    ctx.fit_from_samples(L, np.stack([fld(smp) for fld in fields]), q=q_fit, method=method)
+    I = G.interior_ijk(N)
+    for T in sorted({0, mesh.nt - 1}):
+        got = ctx.eval_stencils(L, T)
+        ref = fields[T](I)
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max(), T
+    ctx.close()
+
+
+def test_fit_affine_macro_gives_the_fem_constant_stencil():
+    """On an unblended (affine) macro every exact stencil is the same
+    (PAPER.md:380-384), so the fitted surrogate equals the FEM stencil at every
+    node and the surrogate apply equals the CONS apply."""
+    mesh, num, Lt, A, cf = oracle_case("flat_tet", 5)
+    ctx = gpu_ctx("flat_tet", 5)
+    sur = ctx.eval_stencils(5, 0, "surrogate")
+    fem_w = ctx.eval_stencils(5, 0, "fem")
+    assert np.abs(sur - fem_w).max() <= 1e-12 * np.abs(fem_w).max()
+    assert np.abs(fem_w - fem_w[0]).max() <= 1e-12 * np.abs(fem_w).max()
+    u, _ = vecs(num)
+    du, dy, dc = to_local(ctx, 5, u), ctx.zeros(5), ctx.zeros(5)
+    ctx.apply(5, du, dy)
+    ctx.apply(5, du, dc, op="const")
+    assert rel(ctx.gather_global(5, dy), ctx.gather_global(5, dc)) < TOL
+
+
+def test_non_positive_centre_weight_raises_numeric():
+    """HHG_ERR_NUMERIC (include/hhg.h): a fitted surrogate whose centre weight
+    is <= 0 somewhere cannot be used by the GS update (it divides by s_mc,
+    eq. iteration-scheme): the fit reports it, apply still
+    works, every smoother call refuses it; a good refit clears it."""
+    import paper_1608_06473_b200 as hhg
+    mesh = synth.single_tet()
+    L = 4
+    ctx = hhg.Ctx.from_mesh(mesh, L)
+    ctx.fit(2)
+    smp = ctx.sample_nodes(L)
+    good = ctx.eval_stencils(L, 0)
+    I = G.interior_ijk(2 ** L)
+    pos = {tuple(p): x for x, p in enumerate(I)}
+    samples = np.stack([good[[pos[tuple(p)] for p in smp]]])
+    bad = samples.copy()
+    bad[0, :, 7] = 1.0 - smp[:, 0] / 4.0          # centre weight linear in i, < 0 for i > 4
+    with pytest.raises(hhg.HHGError) as e:
+        ctx.fit_from_samples(L, bad)
+    assert e.value.status == 4
+    u, f, y = ctx.zeros(L), ctx.zeros(L), ctx.zeros(L)
+    ctx.apply(L, u, y)                              # apply does not divide
+    with pytest.raises(hhg.HHGError) as e:
+        ctx.gs_sweep(L, u, f, 1)
+    assert e.value.status == 4
+    with pytest.raises(hhg.HHGError) as e:
+        ctx.vcycle(L, u, f, n_cycles=1)
+    assert e.value.status == 4
+    ctx.fit_from_samples(L, samples)                # the exact samples again: fine
+    ctx.gs_sweep(L, u, f, 1)
+    ctx.close()
+
+
+@pytest.mark.parametrize("mesh_name,L", [("tet", 7), ("shell480", 5), ("shell60", 4)])
+def test_gs_kernels_bit_identical(mesh_name, L, monkeypatch):
+    """Every volume GS kernel (the persistent sweep and the 4 colour-pass
+    launches) computes the same 4-colour sweep bit for bit (same per-node
+    arithmetic, same colour order)."""
+    mesh, num, *_ = oracle_case(mesh_name, L)
+    ctx = gpu_ctx(mesh_name, L)
+    u, f = vecs(num)
+    du, df = to_local(ctx, L, u), to_local(ctx, L, f)
+    ref = du.clone()
+    monkeypatch.setenv("HHG_GS_KERNEL", "passes")
+    ctx.gs_sweep(L, ref, df, 2)
+    monkeypatch.delenv("HHG_GS_KERNEL")
+    got = du.clone()
+    ctx.gs_sweep(L, got, df, 2)
+    import torch
+    assert torch.equal(got, ref)
+
+
+def test_coarse_cg_through_operator_calls_matches_oracle(monkeypatch):
+    """HHG_COARSE=ops (the coarse solver used for levels too large to
+    replicate, coarse.cu::coarse_replicable): the same 50-iteration CG from
+    zero through the library's operator calls; V(3,3) history as the oracle's
+    to 1e-10."""
+    H = oracle_hierarchy("shell60", 4)
+    num = H.num[4]
+    u0, f = vecs(num, (7, 8))
+    u_ref, hist_ref = H.solve(u0.copy(), f, 2)
+    ctx = gpu_ctx("shell60", 4)
+    monkeypatch.setenv("HHG_COARSE", "ops")
+    du, df = to_local(ctx, 4, u0), to_local(ctx, 4, f)
+    hist = ctx.vcycle(4, du, df, n_cycles=2)
+    assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
+    assert rel(ctx.gather_global(4, du), u_ref) < 1e-10

@@ -4,6 +4,7 @@ import os
 
 import numpy as np
 import pytest
+import scipy.sparse as sp
 
 import synth
 from oracle import geometry as G
@@ -185,3 +186,83 @@ def test_gs_steps_partition_unknowns():
     steps = num.gs_steps()
     allg = np.concatenate(steps)
     assert len(allg) == len(np.unique(allg)) == num.unknown_mask.sum()
+
+
+def test_locate_inverts_gids_and_finds_every_copy():
+    """Numbering.locate(g) lists exactly the (macro, ijk) with gids(T, ijk) == g
+    (brute force over every lattice node of every macro)."""
+    mesh = synth.shell_mesh(0.55, 1.0, 0, 1)
+    N = 4
+    num = G.Numbering(mesh, N)
+    lat = G.lattice_ijk(N)
+    where = {}
+    for T in range(mesh.nt):
+        for x, g in enumerate(num.gids(T, lat)):
+            where.setdefault(int(g), []).append((T, tuple(int(v) for v in lat[x])))
+    for g in range(num.n_total):
+        got = [(T, tuple(int(v) for v in ijk)) for T, ijk in num.locate(g)]
+        assert got == where[g], g
+
+
+def test_step_of_matches_gs_steps():
+    mesh = synth.shell_mesh(0.55, 1.0, 0, 1)
+    num = G.Numbering(mesh, 8)
+    step = -np.ones(num.n_total, dtype=int)
+    for s, ids in enumerate(num.gs_steps()):
+        step[ids] = s
+    for g in range(0, num.n_total, 7):
+        assert num.step_of(g) == step[g], g
+
+
+def test_class_colours_are_independent_inside_each_primitive():
+    """Face colours (s+2t) mod 3 are independent sets inside every face, edge
+    parity classes inside every edge, and vertices are never neighbours (the
+    simultaneous update of one class step is then a true GS step inside each
+    primitive; across primitives it is the Jacobi-like coupling of the hybrid
+    smoother, PAPER.md:853-858)."""
+    from oracle import fem
+    mesh = synth.shell_mesh(0.55, 1.0, 0, 1)
+    N = 8
+    num = G.Numbering(mesh, N)
+    A = fem.assemble(mesh, N, num, blended=True).tocsr()
+    steps = num.gs_steps()
+    for s in range(6):
+        ids = steps[s]
+        if s == 0:
+            groups = [ids]
+        elif s < 3:
+            groups = [ids[(ids - num.base_e) // (N - 1) == e] for e in np.unique((ids - num.base_e) // (N - 1))]
+        else:
+            groups = [ids[(ids - num.base_f) // num.nfi == f] for f in np.unique((ids - num.base_f) // num.nfi)]
+        for grp in groups:
+            sub = A[grp][:, grp]
+            sub = sub - sp.diags(sub.diagonal())
+            assert abs(sub).max() == 0.0 if sub.nnz else True, (s, grp[:4])
+    # and the classes are not globally independent across faces (the hybrid
+    # smoother's Jacobi-like interface couplings exist on this mesh)
+    coupled = 0
+    for s in range(3, 6):
+        sub = A[steps[s]][:, steps[s]]
+        coupled += (sub - sp.diags(sub.diagonal())).nnz
+    assert coupled > 0
+
+
+def test_ipoly_points_are_the_papers():
+    """IPOLY points equal the golden list written out from
+    the paper's formula, are interior, and are the P2 nodes (vertices + edge
+    midpoints) of the shrunk tet with vertices (1,1,1), (a,1,1), (1,a,1),
+    (1,1,a)."""
+    from oracle import surrogate as S
+    rows = _golden("ipoly_points.txt")
+    for L in (3, 4, 5):
+        gold = {tuple(int(x) for x in r[1:]) for r in rows if int(r[0]) == L}
+        pts = {tuple(int(v) for v in p) for p in S.ipoly_samples(L)}
+        assert pts == gold and len(gold) == 10
+        N = 2 ** L
+        for i, j, k in pts:
+            assert i >= 1 and j >= 1 and k >= 1 and i + j + k <= N - 1
+        a = N - 3
+        V = [np.array(v) for v in ((1, 1, 1), (a, 1, 1), (1, a, 1), (1, 1, a))]
+        p2 = {tuple(int(x) for x in v) for v in V}
+        p2 |= {tuple(int(x) for x in (V[p] + V[q]) // 2) for p, q in itertools.combinations(range(4), 2)}
+        assert pts == p2
