@@ -273,6 +273,15 @@ int64_t hhg_kernel_launches(hhg_ctx ctx);
 hhg_status hhg_profile(hhg_ctx ctx, int enable);
 hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, int64_t* launches);
 
+/* Development counters of the single-pass GS kernel: enable != 0 allocates
+ * and zeroes 16 counters that later sweeps accumulate into; out16 (host,
+ * may be NULL) receives them (synchronising) before they are zeroed again:
+ * [0..5] cycles of the first thread of every CTA waiting for planes, in the
+ * node update, waiting for halo words, checking neighbour progress, at the
+ * step barrier and after it; [6] wavefront steps; [7] items; [8] failed halo
+ * polls of all threads.  enable == 0 frees them. */
+hhg_status hhg_gs_prof(hhg_ctx ctx, int enable, unsigned long long* out16);
+
 /* Text of the last error of ctx (owned by ctx, valid until the next call). */
 const char* hhg_last_error(hhg_ctx ctx);
 /* Frees everything ctx owns (device buffers, NCCL communicator, streams,

@@ -43,6 +43,7 @@ def lib():
     P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
     L.hhg_setup_macro_mesh.argtypes = [P, P, I64, P, I64, P, I32, P, I32, I32, P, P, ctypes.POINTER(P)]
     L.hhg_fit_surrogates.argtypes = [P, I32, I32, I32]
+    L.hhg_gs_prof.argtypes = [P, I32, P]
     L.hhg_sample_nodes.argtypes = [P, I32, I32, I32, P, ctypes.POINTER(I64)]
     L.hhg_fit_from_samples.argtypes = [P, I32, I32, I32, I32, P]
     L.hhg_vector_layout.argtypes = [P, I32, ctypes.POINTER(I64), ctypes.POINTER(I64), ctypes.POINTER(I64)]
@@ -219,6 +220,12 @@ class Ctx:
     # ------------------------------------------------------------------
     def fit(self, q=2, method="lsqp", j=2):
         self._check(self._lib.hhg_fit_surrogates(self.h, q, FIT[method], j))
+
+    def gs_prof(self, enable=True, read=False):
+        """Cycle counters of the single-pass GS kernel (hhg_gs_prof)."""
+        out = np.zeros(16, dtype=np.uint64)
+        self._check(self._lib.hhg_gs_prof(self.h, 1 if enable else 0, out.ctypes.data if read else None))
+        return out
 
     def sample_nodes(self, L, method="lsqp", j=2):
         """Sampling set of level L used by the fit (test export), [n, 3] int32."""

@@ -169,6 +169,9 @@ struct Level {
   std::vector<Band> bands;
   Band* d_bands = nullptr;
   int slot_len = 0;
+  std::vector<Band> bands_w;       // <= 2 kMarchThreads columns (single-pass GS, gsfront.cuh)
+  Band* d_bands_w = nullptr;
+  int slot_len_w = 0;
   std::vector<Band> bands_fem;  // element-wise FEM: <= kMarchThreads anchor columns per band
   Band* d_bands_fem = nullptr;
   // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order
@@ -216,6 +219,10 @@ struct Level {
   // persistent GS work queue (k_gs_items)
   int* d_gs_flags = nullptr;   // [nt_local][n_bands][4] sweep epoch of completed colour passes
   int* d_gs_counter = nullptr; // [1]
+  // single-pass wavefront GS (gsfront.cuh), allocated on first use
+  uint64_t* d_gs_ex = nullptr;    // [n_local][2] LL halo words (value halves + epoch tag)
+  uint32_t* d_gs_prog = nullptr;  // [nt_local][n_bands] progress words
+  uint32_t* d_gs_epoch = nullptr; // [1] sweep epoch (incremented on the device per sweep)
   int gs_epoch = 0;
 };
 
@@ -271,6 +278,7 @@ struct Ctx {
   int64_t cg_n = 0;
   double* d_scal = nullptr;           // device scalars
   int* d_flag = nullptr;              // device flag word (fit-time centre-weight check)
+  unsigned long long* d_gsprof = nullptr;  // wavefront GS cycle counters (hhg_gs_prof)
   // profiling (hhg_profile)
   bool prof = false;
   std::vector<cudaEvent_t> ev_pool;

@@ -122,6 +122,41 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
+// GS node value u_I = (f_I - sum_{w != mc} s_w u_w) / s_mc (eq. iteration-scheme,
+// PAPER.md:1306-1315) with s_w(k) = A_w + B_w k + C_w k^2, expanded as
+// x + k (y + k z) over three accumulation chains; shared by every GS kernel
+// (colour passes and the wavefront, gsfront.cuh), so their sweeps are bit-identical.
+// uu[15]: neighbour values in direction order (entry kMC unused).
+template <int OP>
+__device__ __forceinline__ double gs_node_value(const double (&A)[15], const double (&B)[15],
+                                                const double* __restrict__ Cw, int k, const double (&uu)[15],
+                                                double fv) {
+  const double kd = (double)k;
+  const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
+  const double rinv = rcp_nr(smc);
+  double r;
+  if (OP == HHG_OP_SURROGATE) {
+    double x = 0.0, y = 0.0, z = 0.0;
+#pragma unroll
+    for (int w = 0; w < 15; ++w) {
+      if (w == kMC) continue;
+      x = fma(A[w], uu[w], x);
+      y = fma(B[w], uu[w], y);
+      z = fma(Cw[w], uu[w], z);
+    }
+    r = fma(fma(z, kd, y), kd, x);
+  } else {
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int w = 0; w < 15; ++w) {
+      if (w == kMC) continue;
+      acc[w % 3] = fma(A[w], uu[w], acc[w % 3]);
+    }
+    r = (acc[0] + acc[1]) + acc[2];
+  }
+  return (fv - r) * rinv;
+}
+
 // Shared-memory carve-up common to the march kernels (RING plane slots).
 template <int RING = kRing>
 struct MarchSmem {
@@ -360,37 +395,13 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
     const double fv = f_next;
     if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
     if (q.active && k >= 1 && k <= q.len) {
-      const double kd = (double)k;
-      const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(sm.Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
-      const double rinv = rcp_nr(smc);
       const double* Pb = sptr(k - 1);
       const double* Pm = sptr(k);
       const double* Pt = sptr(k + 1);
       const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
                              Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
-      double r;
-      if (OP == HHG_OP_SURROGATE) {
-        // expanded weight polynomial: three independent accumulation chains
-        double x = 0.0, y = 0.0, z = 0.0;
-#pragma unroll
-        for (int w = 0; w < 15; ++w) {
-          if (w == kMC) continue;
-          x = fma(A[w], uu[w], x);
-          y = fma(B[w], uu[w], y);
-          z = fma(sm.Cw[w], uu[w], z);
-        }
-        r = fma(fma(z, kd, y), kd, x);
-      } else {
-        double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int w = 0; w < 15; ++w) {
-          if (w == kMC) continue;
-          acc[w % 3] = fma(A[w], uu[w], acc[w % 3]);
-        }
-        r = (acc[0] + acc[1]) + acc[2];
-      }
-      wb[sm.po[k]] = (fv - r) * rinv;
+      wb[sm.po[k]] = gs_node_value<OP>(A, B, sm.Cw, k, uu, fv);
     }
     // every 3 steps: all warps done with planes <= 4s+2 (next step reads >= 4s+3);
     // refill up to plane 4s+2+RING (the following 3 steps need <= 4s+16; with
@@ -478,36 +489,13 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
     const double fv = f_next;
     if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
     if (q.active && k >= 1 && k <= q.len) {
-      const double kd = (double)k;
-      const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
-      const double rinv = rcp_nr(smc);
       const double* Pb = sptr(k - 1);
       const double* Pm = sptr(k);
       const double* Pt = sptr(k + 1);
       const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
                              Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
-      double r;
-      if (OP == HHG_OP_SURROGATE) {
-        double x = 0.0, y = 0.0, z = 0.0;
-#pragma unroll
-        for (int w = 0; w < 15; ++w) {
-          if (w == kMC) continue;
-          x = fma(A[w], uu[w], x);
-          y = fma(B[w], uu[w], y);
-          z = fma(Cw[w], uu[w], z);
-        }
-        r = fma(fma(z, kd, y), kd, x);
-      } else {
-        double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-        for (int w = 0; w < 15; ++w) {
-          if (w == kMC) continue;
-          acc[w % 3] = fma(A[w], uu[w], acc[w % 3]);
-        }
-        r = (acc[0] + acc[1]) + acc[2];
-      }
-      wb[sm.po[k]] = (fv - r) * rinv;
+      wb[sm.po[k]] = gs_node_value<OP>(A, B, Cw, k, uu, fv);
     }
     GPROF_ADD(6)
     // every 3 steps: all warps done with quads <= s-1 (the next step reads planes >= 4s+3);

@@ -12,6 +12,7 @@
 #include "hhg_internal.h"
 #include "vol_kernels.cuh"
 #include "march.cuh"
+#include "gsfront.cuh"
 #include "gslex.cuh"
 #include "femew.cuh"
 
@@ -359,6 +360,61 @@ static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f)
   return launch_gs_items_r<OP, 24>(c, lv, u, f);
 }
 
+// The whole volume GS (4 colours) as one single-pass wavefront launch
+// (gsfront.cuh): NT threads per CTA over bands of <= NT columns.
+template <int OP, int LAG, int RING, int NT>
+static hhg_status launch_gs_front_r(Ctx* c, Level& lv, double* u, const double* f) {
+  const bool wide = NT > kMarchThreads;
+  const std::vector<Band>& bands = wide ? lv.bands_w : lv.bands;
+  const int slot_len = wide ? lv.slot_len_w : lv.slot_len;
+  const size_t smem = front_smem_bytes<RING, NT>(slot_len, lv.N);
+  if (smem > (size_t)kMaxDynSmem) return HHG_ERR_STATE;
+  const bool prof = c->d_gsprof != nullptr;
+  const void* fn = prof ? (const void*)k_gs_front<OP, LAG, RING, NT, true>
+                        : (const void*)k_gs_front<OP, LAG, RING, NT, false>;
+  hhg_status st = smem_attr(c, fn);
+  if (st != HHG_OK) return st;
+  int grid = 0;
+  if ((st = resident_grid(c, fn, NT, smem, grid)) != HHG_OK) return st;
+  const int nb = (int)bands.size();
+  // every band of the last handed-out macro must be resident (bands of a macro wait on each other)
+  if (grid <= nb) return HHG_ERR_STATE;
+  if (!lv.d_gs_ex) {
+    const size_t np = (size_t)std::max<int64_t>(c->nt_local * (int64_t)lv.bands.size(), 1);
+    HHG_CK(c, cudaMalloc(&lv.d_gs_ex, (size_t)lv.n_local * 2 * sizeof(uint64_t)));
+    HHG_CK(c, cudaMemsetAsync(lv.d_gs_ex, 0, (size_t)lv.n_local * 2 * sizeof(uint64_t), c->stream));
+    HHG_CK(c, cudaMalloc(&lv.d_gs_prog, np * sizeof(uint32_t)));
+    HHG_CK(c, cudaMemsetAsync(lv.d_gs_prog, 0, np * sizeof(uint32_t), c->stream));
+    HHG_CK(c, cudaMalloc(&lv.d_gs_epoch, sizeof(uint32_t)));
+    HHG_CK(c, cudaMemsetAsync(lv.d_gs_epoch, 0, sizeof(uint32_t), c->stream));
+  }
+  const int64_t items = c->nt_local * nb;
+  ProfScope ps(c, 1);
+  k_front_begin<<<1, 1, 0, c->stream>>>(lv.d_gs_counter, lv.d_gs_epoch);
+  HHG_LAUNCHED(c);
+  auto kern = prof ? k_gs_front<OP, LAG, RING, NT, true> : k_gs_front<OP, LAG, RING, NT, false>;
+  kern<<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+      lv.N, lv.S, wide ? lv.d_bands_w : lv.d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local,
+      lv.d_gs_counter, lv.d_gs_epoch, lv.d_gs_prog, lv.d_gs_ex, c->d_gsprof);
+  HHG_LAUNCHED(c);
+  return HHG_OK;
+}
+
+// variant: 0 = 256 threads, LAG 4; 1 = 256, LAG 6; 2 = 512, LAG 4; 3 = 512, LAG 6
+template <int OP>
+static hhg_status launch_gs_front(Ctx* c, Level& lv, double* u, const double* f, int variant) {
+  switch (variant) {
+    case 1: return launch_gs_front_r<OP, 6, 32, kMarchThreads>(c, lv, u, f);
+    case 2: return launch_gs_front_r<OP, 4, 24, 2 * kMarchThreads>(c, lv, u, f);
+    case 3: return launch_gs_front_r<OP, 6, 32, 2 * kMarchThreads>(c, lv, u, f);
+    default:
+      // two CTAs per SM while the 24-slot ring fits half the shared memory
+      if (front_smem_bytes<24, kMarchThreads>(lv.slot_len, lv.N) <= 113 * 1024)
+        return launch_gs_front_r<OP, 4, 24, kMarchThreads>(c, lv, u, f);
+      return launch_gs_front_r<OP, 4, 20, kMarchThreads>(c, lv, u, f);
+  }
+}
+
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
                               const double* f, double* out) {
   if (op == HHG_OP_SURROGATE_FACES) op = HHG_OP_SURROGATE;  // volume rows: the surrogate
@@ -551,14 +607,22 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
     return dist_sync(c, lv, u);
   }
   // HHG_GS_KERNEL (read per call, so tests can compare the variants):
-  // "passes" = 4 colour launches; default = the persistent sweep k_gs_items
+  // default = the persistent 4-pass sweep k_gs_items; the single-pass wavefront
+  // k_gs_front as "front" (256 threads, LAG 4), "front6" (LAG 6), "wide4" /
+  // "wide6" (512 threads); "passes" = 4 colour launches
   const char* e = getenv("HHG_GS_KERNEL");
-  const int mode = (e && std::string(e) == "passes") ? 1 : 2;
+  const std::string ks = e ? e : "";
+  const int mode = ks == "passes" ? 1 : ks == "front" ? 3 : ks == "front6" ? 4 : ks == "wide4" ? 5 : ks == "wide6" ? 6 : 2;
   const bool march_ok = !lv.bands.empty() && ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
   hhg_status st = HHG_ERR_STATE;
   if (march_ok && mode == 2)
     st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
                                 : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
+  if (march_ok && mode >= 3) {
+    const int variant = mode - 3;
+    st = op == HHG_OP_SURROGATE ? launch_gs_front<HHG_OP_SURROGATE>(c, lv, u, f, variant)
+                                : launch_gs_front<HHG_OP_CONST_AFFINE>(c, lv, u, f, variant);
+  }
   if (st != HHG_OK) {
     if (c->poisoned) return HHG_ERR_CUDA;
     for (int col = 0; col < 4; ++col)
@@ -748,6 +812,27 @@ extern "C" hhg_status hhg_eval_stencils(hhg_ctx ctx, int L, hhg_op op, int64_t m
   if (so.staged) {
     HHG_CK(c, cudaMemcpyAsync(out, so.dev, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
+  }
+  return HHG_OK;
+}
+
+// Cycle accounting of the wavefront GS kernel (development): enable != 0
+// allocates and zeroes the counters, later sweeps accumulate; read copies the
+// 16 counters out (thread 0's cycles in mbar wait / compute / halo wait /
+// progress check / barrier / post-barrier, steps, items, failed halo polls).
+extern "C" hhg_status hhg_gs_prof(hhg_ctx ctx, int enable, unsigned long long* out16) {
+  Ctx* c = (Ctx*)ctx;
+  if (!c) return HHG_ERR_INVALID;
+  if (enable && !c->d_gsprof) HHG_CK(c, cudaMalloc(&c->d_gsprof, 16 * sizeof(unsigned long long)));
+  if (out16 && c->d_gsprof) {
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    HHG_CK(c, cudaMemcpy(out16, c->d_gsprof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+  }
+  if (c->d_gsprof) HHG_CK(c, cudaMemsetAsync(c->d_gsprof, 0, 16 * sizeof(unsigned long long), c->stream));
+  if (!enable && c->d_gsprof) {
+    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    cudaFree(c->d_gsprof);
+    c->d_gsprof = nullptr;
   }
   return HHG_OK;
 }

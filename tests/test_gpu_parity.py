@@ -449,23 +449,30 @@ def test_non_positive_centre_weight_raises_numeric():
     ctx.close()
 
 
-@pytest.mark.parametrize("mesh_name,L", [("tet", 7), ("shell480", 5), ("shell60", 4)])
-def test_gs_kernels_bit_identical(mesh_name, L, monkeypatch):
-    """Every volume GS kernel (the persistent sweep and the 4 colour-pass
-    launches) computes the same 4-colour sweep bit for bit (same per-node
-    arithmetic, same colour order)."""
+@pytest.mark.parametrize("kernel", ["front", "front6", "wide4", "wide6", "default"])
+@pytest.mark.parametrize("mesh_name,L", [("tet", 7), ("shell480", 5), ("shell60", 4), ("tet", 3)])
+def test_gs_kernels_bit_identical(mesh_name, L, kernel, monkeypatch):
+    """Every volume GS kernel -- the persistent 4-pass sweep (default), the
+    single-pass wavefronts ("front", "front6", "wide4", "wide6") and the 4
+    colour launches ("passes", the reference here) -- computes the same
+    4-colour sweep bit for bit (same per-node arithmetic gs_node_value, same
+    colour order); surrogate and constant-stencil smoothers."""
+    import torch
     mesh, num, *_ = oracle_case(mesh_name, L)
     ctx = gpu_ctx(mesh_name, L)
     u, f = vecs(num)
     du, df = to_local(ctx, L, u), to_local(ctx, L, f)
-    ref = du.clone()
-    monkeypatch.setenv("HHG_GS_KERNEL", "passes")
-    ctx.gs_sweep(L, ref, df, 2)
-    monkeypatch.delenv("HHG_GS_KERNEL")
-    got = du.clone()
-    ctx.gs_sweep(L, got, df, 2)
-    import torch
-    assert torch.equal(got, ref)
+    for op in ("surrogate", "const"):
+        ref = du.clone()
+        monkeypatch.setenv("HHG_GS_KERNEL", "passes")
+        ctx.gs_sweep(L, ref, df, 2, op=op)
+        if kernel == "default":
+            monkeypatch.delenv("HHG_GS_KERNEL")
+        else:
+            monkeypatch.setenv("HHG_GS_KERNEL", kernel)
+        got = du.clone()
+        ctx.gs_sweep(L, got, df, 2, op=op)
+        assert torch.equal(got, ref), (op, (got - ref).abs().max().item())
 
 
 def test_coarse_cg_through_operator_calls_matches_oracle(monkeypatch):

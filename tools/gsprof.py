@@ -1,32 +1,57 @@
-"""Cycle breakdown of the quad GS kernel (instrumented build tools/prof/libhhg_prof.so)."""
-import ctypes, os, sys
+"""Cycle accounting of the single-pass GS kernel (hhg_gs_prof) on the bench
+workload: where the first thread of every CTA spends a wavefront step.
+
+usage: python tools/gsprof.py [t] [n_r] [L] [reps]
+"""
+import os
+import sys
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+
+import numpy as np
+import torch
+
 import paper_1608_06473_b200 as hhg
-hhg.LIB_PATH = os.path.join(ROOT, "tools", "prof", "libhhg_prof.so")
-import numpy as np, torch, synth
-os.environ.setdefault("HHG_GS_KERNEL", "items")
-mesh = synth.shell_mesh(0.55, 1.0, 1, 2)
-L = 7
-ctx = hhg.Ctx.from_mesh(mesh, L)
-ctx.fit(2)
-n_local, n_owned, n_global = ctx.layout(L)
-g = np.arange(n_global)
-u, f = ctx.zeros(L), ctx.zeros(L)
-ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(0, g)).cuda(), u)
-ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(1, g)).cuda(), f)
-lib = hhg.lib()
-buf = (ctypes.c_ulonglong * 12)()
-ctx.gs_sweep(L, u, f, 1); torch.cuda.synchronize(); lib.hhg_gs_prof_read(buf)
-ctx.gs_sweep(L, u, f, 1); torch.cuda.synchronize(); lib.hhg_gs_prof_read(buf)
-v = list(buf)
-tot = v[3]
-if os.environ["HHG_GS_KERNEL"] == "quad":
-    print("CTA-cycles total %.3e, data-wait %.1f%%, barrier %.1f%%, item-start %.1f%%, quads %d, cycles/quad/CTA %.0f" % (
-        tot, 100 * v[0] / tot, 100 * v[1] / tot, 100 * v[2] / tot, v[4], tot / max(v[4], 1)))
-else:
-    print("items: CTA-cycles total %.3e: flag waits %.1f%%, passes %.1f%% (of which refill issue %.1f%%, "
-          "quad waits %.1f%%, node compute %.1f%%, refill barrier %.1f%%, pass start %.1f%%, final waits %.1f%%, "
-          "end barrier %.1f%%), item setup %.1f%%" % (
-              tot, 100 * v[0] / tot, 100 * v[1] / tot, 100 * v[2] / tot, 100 * v[5] / tot, 100 * v[6] / tot,
-              100 * v[7] / tot, 100 * v[8] / tot, 100 * v[9] / tot, 100 * v[10] / tot, 100 * v[4] / tot))
+import synth
+
+if os.environ.get("KB_LIB"):  # variant build of the library (tools/build_variant.py)
+    hhg.LIB_PATH = os.path.abspath(os.environ["KB_LIB"])
+
+
+def main():
+    t = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+    nr = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    L = int(sys.argv[3]) if len(sys.argv) > 3 else 7
+    reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
+    mesh = synth.shell_mesh(0.55, 1.0, t, nr)
+    ctx = hhg.Ctx.from_mesh(mesh, L)
+    ctx.fit(2)
+    n_local, n_owned, n_global = ctx.layout(L)
+    g = np.arange(n_global)
+    u, f = ctx.zeros(L), ctx.zeros(L)
+    ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(0, g)).cuda(), u)
+    ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(1, g)).cuda(), f)
+    ctx.gs_sweep(L, u, f, 1)
+    ctx.gs_prof(True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    ctx.gs_sweep(L, u, f, reps)
+    e1.record()
+    torch.cuda.synchronize()
+    c = ctx.gs_prof(True, read=True).astype(np.float64)
+    ctx.gs_prof(False)
+    steps = c[6]
+    names = ["plane wait", "node update", "halo wait", "progress", "barrier", "post-barrier"]
+    tot = c[:6].sum()
+    tag = os.environ.get("KB_TAG", os.environ.get("HHG_GS_KERNEL", "default"))
+    print(f"{tag}: {e0.elapsed_time(e1) / reps:.3f} ms/sweep (whole call), items {c[7] / reps:.0f}, "
+          f"steps/item {steps / max(c[7], 1):.1f}, cycles/step {tot / max(steps, 1):.0f}, "
+          f"failed halo polls/step/CTA {c[8] / max(steps, 1):.1f}")
+    for x, n in enumerate(names):
+        print(f"   {n:13s} {c[x] / max(steps, 1):8.0f} cyc/step  {100 * c[x] / max(tot, 1):5.1f} %")
+    ctx.close()
+
+
+if __name__ == "__main__":
+    main()
