@@ -87,6 +87,32 @@ hhg_status face_centre_check(Ctx* c, Level& lv, int* d_flag) {
   return HHG_OK;
 }
 
+// Operands of a face row in summation order: un[e] = u at neighbour e
+// (entries 1..6 in-face, then the 4 into-macro entries of the macro with the
+// LOWER global id, then the other 4; 0 where a neighbour is absent), wv[e] the
+// matching weights (wv[0] = centre).  The canonical order makes the row's
+// rounding independent of which macro is local where (bitwise-equal results on
+// any number of ranks).
+template <class W>
+__device__ __forceinline__ void face_row_operands(const FaceLP& F, const FaceRowSlots& o,
+                                                  const double* __restrict__ u, W wgt, double (&un)[14],
+                                                  double (&wv)[15]) {
+#pragma unroll
+  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
+#pragma unroll
+  for (int e = 0; e < 15; ++e) wv[e] = (e == 0 || o.nb[e - 1] >= 0) ? wgt(e) : 0.0;
+  if (F.bfirst) {
+#pragma unroll
+    for (int e = 6; e < 10; ++e) {
+      const double a = un[e], w = wv[e + 1];
+      un[e] = un[e + 4];
+      wv[e + 1] = wv[e + 5];
+      un[e + 4] = a;
+      wv[e + 5] = w;
+    }
+  }
+}
+
 // mode: kModeApply / kModeResid (vol_kernels.cuh values 0 / 1)
 __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, const FaceLP* __restrict__ flp,
                              const uint32_t* __restrict__ fst, const int* __restrict__ po,
@@ -106,28 +132,13 @@ __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, con
   auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
     return fcoef ? face_poly(fcoef + (fc * 15 + e) * nfc, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
   };
-  double acc;
-  if (fcoef) {  // all neighbour values first (memory-level parallelism), then the weights
-    double un[14];
+  // every gather and weight first (memory-level parallelism: the face rows
+  // are latency-bound, ncu r01h: long-scoreboard 74 %), then the fma chain
+  double un[14], wv[15];
+  face_row_operands(F, o, u, wgt, un, wv);
+  double acc = wv[0] * u[o.cA];
 #pragma unroll
-    for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
-    acc = wgt(0) * u[o.cA];
-#pragma unroll
-    for (int e = 0; e < 14; ++e) acc = fma(wgt(e + 1), un[e], acc);
-  } else {
-    // every gather and weight load first (memory-level parallelism: the face
-    // rows are latency-bound, ncu r01h: long-scoreboard 74 %), then the same
-    // fma chain (apply 0.52 -> 0.48 ms; GS unchanged)
-    double un[14], wv[15];
-#pragma unroll
-    for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
-#pragma unroll
-    for (int e = 0; e < 15; ++e) wv[e] = val[e * n_frows + r];
-    acc = wv[0] * u[o.cA];
-#pragma unroll
-    for (int e = 0; e < 14; ++e)
-      if (o.nb[e] >= 0) acc = fma(wv[e + 1], un[e], acc);
-  }
+  for (int e = 0; e < 14; ++e) acc = fma(wv[e + 1], un[e], acc);
   const double res = mode == 1 ? f[o.cA] - acc : acc;
   out[o.cA] = res;
   if (o.cB >= 0) out[o.cB] = res;
@@ -164,26 +175,12 @@ __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, co
   auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
     return fcoef ? face_poly(fcoef + (fc * 15 + e) * ncf, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
   };
+  double un[14], wv[15];
+  face_row_operands(F, o, u, wgt, un, wv);
   double acc = f[o.cA];
-  double v;
-  if (fcoef) {  // all neighbour values first (memory-level parallelism), then the weights
-    double un[14];
 #pragma unroll
-    for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
-#pragma unroll
-    for (int e = 0; e < 14; ++e) acc = fma(-wgt(e + 1), un[e], acc);
-    v = acc / wgt(0);
-  } else {
-    double un[14], wv[15];
-#pragma unroll
-    for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
-#pragma unroll
-    for (int e = 0; e < 15; ++e) wv[e] = val[e * n_frows + r];
-#pragma unroll
-    for (int e = 0; e < 14; ++e)
-      if (o.nb[e] >= 0) acc = fma(-wv[e + 1], un[e], acc);
-    v = acc / wv[0];
-  }
+  for (int e = 0; e < 14; ++e) acc = fma(-wv[e + 1], un[e], acc);
+  const double v = acc / wv[0];
   if (face_inner(N, st & 0xffff, st >> 16)) {
     u[o.cA] = v;
     if (o.cB >= 0) u[o.cB] = v;

@@ -44,13 +44,15 @@ hhg_status launch_fem_partial(Ctx* c, int L, const uint32_t* d_slots, int64_t n,
 __global__ void k_lp_values(const double* __restrict__ geo, int N, int64_t S, int64_t n_rows,
                             const uint64_t* __restrict__ row_ptr,
                             const uint64_t* __restrict__ copy_ptr,
-                            const uint32_t* __restrict__ copy, const uint8_t* __restrict__ cmap,
-                            bool blended, double* __restrict__ val) {
+                            const uint32_t* __restrict__ copy, const uint32_t* __restrict__ cord,
+                            const uint8_t* __restrict__ cmap, bool blended, double* __restrict__ val) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= n_rows) return;
   uint64_t e0 = row_ptr[r], e1 = row_ptr[r + 1];
   for (uint64_t e = e0; e < e1; ++e) val[e] = 0.0;
-  for (uint64_t cc = copy_ptr[r]; cc < copy_ptr[r + 1]; ++cc) {
+  // copies in canonical order (cord: global macro id), so the sums are partition-independent
+  for (uint64_t x = copy_ptr[r]; x < copy_ptr[r + 1]; ++x) {
+    const uint64_t cc = cord[x];
     uint32_t s = copy[cc];
     int64_t T = s / S;
     int i, j, k;
@@ -64,20 +66,24 @@ __global__ void k_lp_values(const double* __restrict__ geo, int N, int64_t S, in
   }
 }
 
-hhg_status build_lp_values(Ctx* c, Level& lv, const std::vector<uint8_t>& cmap) {
+hhg_status build_lp_values(Ctx* c, Level& lv, const std::vector<uint8_t>& cmap, const std::vector<uint32_t>& cord) {
   if (lv.n_rows == 0) return HHG_OK;
   uint8_t* d_cmap = nullptr;
+  uint32_t* d_cord = nullptr;
   HHG_CK(c, cudaMalloc(&d_cmap, cmap.size()));
   HHG_CK(c, cudaMemcpyAsync(d_cmap, cmap.data(), cmap.size(), cudaMemcpyHostToDevice, c->stream));
+  HHG_CK(c, cudaMalloc(&d_cord, cord.size() * sizeof(uint32_t)));
+  HHG_CK(c, cudaMemcpyAsync(d_cord, cord.data(), cord.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
   unsigned grid = (unsigned)((lv.n_rows + 127) / 128);
   k_lp_values<<<grid, 128, 0, c->stream>>>(c->d_geo, lv.N, lv.S, lv.n_rows, lv.d_row_ptr,
-                                          lv.d_copy_ptr, lv.d_copy, d_cmap, true, lv.d_val);
+                                          lv.d_copy_ptr, lv.d_copy, d_cord, d_cmap, true, lv.d_val);
   HHG_LAUNCHED(c);
   k_lp_values<<<grid, 128, 0, c->stream>>>(c->d_geo, lv.N, lv.S, lv.n_rows, lv.d_row_ptr,
-                                          lv.d_copy_ptr, lv.d_copy, d_cmap, false, lv.d_val_cons);
+                                          lv.d_copy_ptr, lv.d_copy, d_cord, d_cmap, false, lv.d_val_cons);
   HHG_LAUNCHED(c);
   HHG_CK(c, cudaStreamSynchronize(c->stream));
   HHG_CK(c, cudaFree(d_cmap));
+  HHG_CK(c, cudaFree(d_cord));
   return HHG_OK;
 }
 

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
                const double* __restrict__ f, int64_t ntl, int* __restrict__ counter,
                const uint32_t* __restrict__ epoch_ptr, uint32_t* __restrict__ prog, uint64_t* __restrict__ ex,
-               unsigned long long* __restrict__ gprof) {
+               unsigned long long* __restrict__ gprof, int stress) {
   static_assert(LAG % 2 == 0 && LAG >= 4, "LAG even, >= 4 (DELTA = LAG - 2 >= 2 steps of slack)");
   // plane t + 1 + DELTA is waited at step t and issued at the end of step
   // t + 1 + DELTA - RING + 3 LAG + 1: at least one step earlier
@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const int64_t item = s_item;
     if (item >= total) break;
     const int64_t T = item / n_bands;
-    const int band = (int)(item - T * n_bands);
+    // stress test (HHG_GS_STRESS): bands of a macro in reverse order, random delays
+    const int band = (stress & 1) ? n_bands - 1 - (int)(item - T * n_bands) : (int)(item - T * n_bands);
     const Band b = bands[band];
     if (threadIdx.x == 0) {
       it.TS = T * S;
@@ -335,6 +336,10 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
         it.known_lo = klo;
         it.known_hi = khi;
+      }
+      if (stress) {
+        const uint32_t h = stress_hash(stress, (uint32_t)(it.TS + t), threadIdx.x);
+        if ((h & 63) == 0) __nanosleep((h >> 8) & 4095);
       }
       mark(3);
       __syncthreads();

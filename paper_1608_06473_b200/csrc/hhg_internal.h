@@ -125,6 +125,7 @@ struct FaceLP {
   int8_t off[14][3];    // ijk offsets: [0..5] in-face (A frame), [6..9] into A, [10..13] into B (B frame)
   int8_t mapA[15], mapB[15];  // partial-stencil direction -> entry (-1: not a neighbour)
   int8_t z;             // in-face row mode: node order q -> (s,t) from table fst[z] (setup.cu)
+  int8_t bfirst;        // 1: macro B has the lower global id (its entries are summed first)
   int64_t fid;          // canonical face id
 };
 
@@ -256,7 +257,7 @@ struct Ctx {
   std::vector<int64_t> tets;
   std::vector<uint8_t> dirichlet;
   std::vector<int64_t> local_macros;  // global ids of local macros
-  std::vector<MacroTopo> topo;        // [nt_local]
+  std::vector<MacroTopo> topo;        // [nt_blocks] (local macros, then ghosts)
   MacroTopo* d_topo = nullptr;
   double* d_geo = nullptr;            // [nt_local][4][4]: x,y,z,r per local vertex
   std::vector<Level> levels;          // index L
@@ -378,6 +379,6 @@ hhg_status dist_allreduce_vec(Ctx* c, double* d_vec, int64_t n);
 // Device geometry helpers (fem.cu)
 hhg_status launch_fem_partial(Ctx* c, int L, const uint32_t* d_slots, int64_t n, bool blended,
                               double* d_out15);
-hhg_status build_lp_values(Ctx* c, Level& lv, const std::vector<uint8_t>& cmap);
+hhg_status build_lp_values(Ctx* c, Level& lv, const std::vector<uint8_t>& cmap, const std::vector<uint32_t>& cord);
 
 }  // namespace hhg

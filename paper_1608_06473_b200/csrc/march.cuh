@@ -66,6 +66,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Delays of the protocol stress tests (HHG_GS_STRESS): a 32-bit hash.
+__device__ __forceinline__ uint32_t stress_hash(uint32_t seed, uint32_t a, uint32_t b) {
+  uint32_t h = seed * 0x9e3779b9u ^ (a + 0x7f4a7c15u) * 0x85ebca6bu ^ (b + 0x165667b1u) * 0xc2b2ae35u;
+  h ^= h >> 15;
+  h *= 0x2c1b3c6du;
+  h ^= h >> 12;
+  return h;
+}
+
 // Upper bound of a cross-CTA wait (polls of >= 32 ns: > 1 s) before it traps.
 constexpr long long kSpinLimit = 1ll << 25;
 
@@ -574,7 +583,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
                const double* __restrict__ f, int64_t ntl, int* __restrict__ counter, int* __restrict__ flags,
-               int epoch) {
+               int epoch, int stress) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem<RING> sm(smem, slot_len);
   __shared__ int s_item;
@@ -589,7 +598,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     __syncthreads();
     if (item >= total) break;
     const int64_t T = item / n_bands;
-    const int band = (int)(item - T * n_bands);
+    // stress test (HHG_GS_STRESS): bands of a macro handed out in reverse order
+    // (macro-major order kept: still deadlock-free) and random delays below
+    const int band = (stress & 1) ? n_bands - 1 - (int)(item - T * n_bands) : (int)(item - T * n_bands);
     const double* const Cw = sm.Cw;
     const Band b = bands[band];
     Column q;
@@ -615,6 +626,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
           }
         }
       }
+      if (stress && threadIdx.x == 0) __nanosleep(stress_hash(stress, (uint32_t)(T * n_bands + band), colour) & 8191);
       __syncthreads();
       // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
       // neighbours' generic global writes before their async-proxy reads

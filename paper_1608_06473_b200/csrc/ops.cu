@@ -325,6 +325,13 @@ static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, cons
   return HHG_OK;
 }
 
+// HHG_GS_STRESS=<seed> (tests): the persistent GS kernels hand out the bands of
+// a macro in reverse order and insert random delays (read per call).
+static int gs_stress() {
+  const char* e = getenv("HHG_GS_STRESS");
+  return e ? atoi(e) : 0;
+}
+
 // The whole volume GS (4 colours) as one persistent launch (march.cuh::k_gs_items).
 template <int OP, int RING>
 static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* f) {
@@ -348,7 +355,7 @@ static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* 
   ProfScope ps(c, 1);
   k_gs_items<OP, kMarchThreads, RING><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
       lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter,
-      lv.d_gs_flags, lv.gs_epoch);
+      lv.d_gs_flags, lv.gs_epoch, gs_stress());
   HHG_LAUNCHED(c);
   return HHG_OK;
 }
@@ -395,7 +402,7 @@ static hhg_status launch_gs_front_r(Ctx* c, Level& lv, double* u, const double* 
   auto kern = prof ? k_gs_front<OP, LAG, RING, NT, true> : k_gs_front<OP, LAG, RING, NT, false>;
   kern<<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
       lv.N, lv.S, wide ? lv.d_bands_w : lv.d_bands, nb, slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local,
-      lv.d_gs_counter, lv.d_gs_epoch, lv.d_gs_prog, lv.d_gs_ex, c->d_gsprof);
+      lv.d_gs_counter, lv.d_gs_epoch, lv.d_gs_prog, lv.d_gs_ex, c->d_gsprof, gs_stress());
   HHG_LAUNCHED(c);
   return HHG_OK;
 }

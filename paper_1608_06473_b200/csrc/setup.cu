@@ -128,6 +128,7 @@ static hhg_status build_face_rows(Ctx* c, Topology& tp, Level& lv) {
         if ((la == 1 || la == 2) && (lb == 0 || lb == 3)) std::swap(F.TA, F.TB);
       }
     }
+    F.bfirst = (int8_t)(F.TB >= 0 && c->topo[F.TB].gT < c->topo[F.TA].gT);
     for (int side = 0; side < 2; ++side) {
       const int T = side == 0 ? F.TA : F.TB;
       int8_t* l = side == 0 ? F.lA : F.lB;
@@ -399,17 +400,31 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   }
   lv.nnz = (int64_t)rp[nr];
   lv.n_copies = (int64_t)cp[nr];
-  std::vector<uint32_t> col(lv.nnz), copy(lv.n_copies);
+  std::vector<uint32_t> col(lv.nnz), copy(lv.n_copies), cord(lv.n_copies);
   std::vector<int64_t> rgid(nr);
   std::vector<uint8_t> cmap(lv.n_copies * 16, 255);
   bool overflow = false;
+  // The copies of a row are stored in local block order (the first is read as
+  // the row's own value), but the row's columns are discovered -- and its
+  // partial stencils summed (cord, k_lp_values) -- in the CANONICAL order of
+  // the copies (global macro id, then i, j, k): the row's entries and their
+  // rounding are then the same on every partition (bitwise-equal results on
+  // any number of ranks).
 #pragma omp parallel
   {
     std::vector<std::array<int, 4>> cps;
     std::vector<int64_t> cols;
+    std::vector<int> perm;
 #pragma omp for schedule(dynamic, 4096)
     for (int64_t r = 0; r < nr; ++r) {
       copies_of(rows[r], cps);
+      perm.resize(cps.size());
+      for (size_t q = 0; q < cps.size(); ++q) perm[q] = (int)q;
+      std::sort(perm.begin(), perm.end(), [&](int a, int b) {
+        const int64_t ga = c->topo[cps[a][0]].gT, gb = c->topo[cps[b][0]].gT;
+        if (ga != gb) return ga < gb;
+        return cps[a] < cps[b];
+      });
       cols.clear();
       rgid[r] = row_gid(rows[r]);
       cols.push_back(rgid[r]);
@@ -417,8 +432,13 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
       col[e0] = (uint32_t)slot_of(cps[0][0], cps[0][1], cps[0][2], cps[0][3]);
       for (size_t q = 0; q < cps.size(); ++q) {
         auto& cpy = cps[q];
+        copy[cp[r] + q] = (uint32_t)slot_of(cpy[0], cpy[1], cpy[2], cpy[3]);
+        cord[cp[r] + q] = (uint32_t)(cp[r] + perm[q]);
+      }
+      for (size_t qq = 0; qq < cps.size(); ++qq) {
+        const size_t q = (size_t)perm[qq];
+        auto& cpy = cps[q];
         uint64_t ci = cp[r] + q;
-        copy[ci] = (uint32_t)slot_of(cpy[0], cpy[1], cpy[2], cpy[3]);
         cmap[ci * 16 + kMC] = 0;
         for (int w = 0; w < 15; ++w) {
           if (w == kMC) continue;
@@ -579,7 +599,7 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   HHG_CK(c, cudaMalloc(&lv.d_val_cons, std::max<int64_t>(lv.nnz, 1) * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_tmp, std::max<int64_t>(nr, 1) * sizeof(double)));
   HHG_CK(c, cudaMalloc(&lv.d_cons, c->nt_local * 15 * sizeof(double)));
-  if ((st = build_lp_values(c, lv, cmap)) != HHG_OK) return st;
+  if ((st = build_lp_values(c, lv, cmap, cord)) != HHG_OK) return st;
   // constant (affine) stencil per macro: interior node (1,1,1)
   {
     std::vector<uint32_t> sl(c->nt_local);

@@ -169,3 +169,91 @@ def test_two_rank_vcycle_matches_oracle(mesh_args, L, cycles, world, part):
         assert np.all(np.abs(res[r]["hist"] - hist_ref) <= 1e-10 * hist_ref), (r, res[r]["hist"], hist_ref)
     rel = np.linalg.norm(res[0]["u"] - u_ref) / np.linalg.norm(u_ref)
     assert rel < 1e-10
+
+
+def _bworker(rank, world, port, mesh_args, L, out_q, part):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import paper_1608_06473_b200 as hhg
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        mesh = synth.shell_mesh(0.55, 1.0, *mesh_args)
+        if world > 1:
+            hhg.set_torch_transport(host_only=False)
+            owner = (hhg.partition_rcb(mesh.vertices, mesh.tets, world) if part == "rcb"
+                     else (np.arange(mesh.nt) * world) // mesh.nt)
+            ctx = hhg.Ctx.from_mesh(mesh, L, rank=rank, nranks=world, owner=owner)
+        else:
+            ctx = hhg.Ctx.from_mesh(mesh, L)
+        ctx.fit(2)
+        n_local, n_owned, n_global = ctx.layout(L)
+        g = np.arange(n_global)
+        num = G.Numbering(mesh, 2 ** L)
+        u = synth.uniform_pm1(0, g) * num.unknown_mask
+        f = synth.uniform_pm1(1, g) * num.unknown_mask
+        du, df, dy, dr = ctx.zeros(L), ctx.zeros(L), ctx.zeros(L), ctx.zeros(L)
+        ctx.scatter_global(L, torch.from_numpy(u).cuda(), du)
+        ctx.scatter_global(L, torch.from_numpy(f).cuda(), df)
+        ctx.apply(L, du, dy)
+        nrm = ctx.residual(L, du, df, dr, norm=True)
+        ug = du.clone()
+        ctx.gs_sweep(L, ug, df, 2)
+        hist = ctx.vcycle(L, du, df, n_cycles=2)
+        torch.cuda.synchronize()
+        out = {"norm": nrm, "hist": hist}
+        for name, vec in (("y", dy), ("r", dr), ("ug", ug), ("uv", du)):
+            v = torch.from_numpy(ctx.gather_global(L, vec))
+            if world > 1:
+                dist.all_reduce(v)  # each entry owned by exactly one rank (+0.0 elsewhere: exact)
+            out[name] = v.numpy()
+        out_q.put((rank, out))
+        ctx.close()
+    except Exception:  # pragma: no cover
+        import traceback
+        out_q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, mesh_args, L, part):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bworker, args=(r, world, port, mesh_args, L, q, part)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=900) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+    return res
+
+
+@pytest.mark.parametrize("part", ["rcb", "contig"])
+def test_results_bitwise_identical_across_rank_counts(part):
+    """apply, residual and GS sweeps give BITWISE the same
+    vectors on 1, 2, 3 and 4 ranks (every node's arithmetic is partition-
+    independent: volume rows per macro, lower-primitive rows at their owner
+    from the same stored rows); the residual norm and the V(3,3) history
+    (sums over rank partials) agree to 1e-14 / 1e-12 and the V-cycle iterate
+    to 1e-12."""
+    mesh_args, L = (0, 2), 4
+    ref = _run(1, mesh_args, L, part)[0]
+    for world in (2, 3, 4):
+        res = _run(world, mesh_args, L, part)
+        for r in range(world):
+            o = res[r]
+            for name in ("y", "r", "ug"):
+                assert np.array_equal(o[name], ref[name]), (world, r, name, np.abs(o[name] - ref[name]).max())
+            assert abs(o["norm"] - ref["norm"]) <= 1e-14 * ref["norm"], (world, o["norm"], ref["norm"])
+            assert np.all(np.abs(o["hist"] - ref["hist"]) <= 1e-12 * ref["hist"]), (world, o["hist"], ref["hist"])
+            rel = np.linalg.norm(o["uv"] - ref["uv"]) / np.linalg.norm(ref["uv"])
+            assert rel < 1e-12, (world, rel)

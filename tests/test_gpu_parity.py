@@ -490,3 +490,31 @@ def test_coarse_cg_through_operator_calls_matches_oracle(monkeypatch):
     hist = ctx.vcycle(4, du, df, n_cycles=2)
     assert np.all(np.abs(hist - hist_ref) <= 1e-10 * hist_ref), (hist, hist_ref)
     assert rel(ctx.gather_global(4, du), u_ref) < 1e-10
+
+
+@pytest.mark.parametrize("kernel", ["default", "front", "wide4"])
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("mesh_name,L", [("tet", 7), ("shell480", 5)])
+def test_gs_flag_protocol_stress(mesh_name, L, seed, kernel, monkeypatch):
+    """Stress of the cross-CTA protocols of the persistent GS kernels
+    (completion flags of the 4-pass sweep; LL halo words and progress words of
+    the wavefront, PAPER.md:1306-1315 update order): bands of every macro
+    handed out in reverse order (odd seeds) and random delays of up to ~8 us
+    before passes / steps -- the sweep stays bit-identical to the 4 colour
+    launches, which have no cross-CTA waits at all."""
+    import torch
+    mesh, num, *_ = oracle_case(mesh_name, L)
+    ctx = gpu_ctx(mesh_name, L)
+    u, f = vecs(num)
+    du, df = to_local(ctx, L, u), to_local(ctx, L, f)
+    ref = du.clone()
+    monkeypatch.setenv("HHG_GS_KERNEL", "passes")
+    ctx.gs_sweep(L, ref, df, 2)
+    if kernel == "default":
+        monkeypatch.delenv("HHG_GS_KERNEL")
+    else:
+        monkeypatch.setenv("HHG_GS_KERNEL", kernel)
+    monkeypatch.setenv("HHG_GS_STRESS", str(seed))
+    got = du.clone()
+    ctx.gs_sweep(L, got, df, 2)
+    assert torch.equal(got, ref)

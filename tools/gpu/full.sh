@@ -1,0 +1,2 @@
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout 2700 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/gputest.log 2>&1; echo rc=$? >> gpurun_out/gputest.log
