@@ -29,6 +29,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "GLUP/s surrogate stencil apply + GS sweep (fp64) at 1/2/4/8 B200; % HBM roofline"
 UNIT = "GLUP/s"
+# fp64 floor of the apply: 45 DFMA per volume unknown (15 weights x 2 + 15,
+# SURVEY 8(d)); peak measured by tools/peak_fp64.cu on a B200 at 1965 MHz
+DFMA_PER_UNKNOWN = 45
+DFMA_PER_S = 148 * 58.8 * 1965e6
 
 
 def parse():
@@ -312,6 +316,22 @@ def main():
                 "share_of_step": tot_ms / (ms * a.steps),
                 "apply_frac": nvol * 16 * a.steps / (va_ms * 1e-3) / 1e9 / hbm,
                 "gs_frac": (nvol * 24 * a.steps / (vg_ms * 1e-3) / 1e9 / hbm) if vg_n else None}
+        # the apply is HBM- AND fp64-bound: 16 B and 45 DFMA per
+        # volume unknown; its roofline time is the larger of the two floors
+        t_apply = va_ms * 1e-3 / a.steps
+        t_hbm = nvol * 16 / (hbm * 1e9)
+        t_fp64 = nvol * DFMA_PER_UNKNOWN / (DFMA_PER_S * (clk.summary().get("sm_mhz") or 1965.0) / 1965.0)
+        roof["apply_roofline"] = {"bound": "fp64" if t_fp64 > t_hbm else "hbm", "t_hbm_ms": t_hbm * 1e3,
+                                  "t_fp64_ms": t_fp64 * 1e3, "t_measured_ms": t_apply * 1e3,
+                                  "frac": max(t_hbm, t_fp64) / t_apply,
+                                  "fp64_peak_dfma_per_s": DFMA_PER_S,
+                                  "fp64_peak_source": "tools/peak_fp64.cu on a B200 (58.8 DFMA/clk/SM at 1965 MHz)"}
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            roof["fp64_pipe_pct"] = {k: v.get("fp64_pipe_pct") for k, v in tr.items()
+                                     if isinstance(v, dict) and v.get("fp64_pipe_pct") is not None}
+        except Exception:
+            pass
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -345,6 +365,8 @@ def main():
                 out["comparisons"].update(other_configs(stream, q))
     if rank == 0 and not a.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(L, q)
+        if ws == 1:
+            out["cpu_baseline"]["parity_of_timed_step"] = step_parity(ctx, mesh, L, q, u, f, y, step)
     if rank == 0:
         print(json.dumps(out), flush=True)
     ctx.close()
@@ -374,10 +396,26 @@ def e2e(ctx, L, u, f, y, a, n_owned, tmax):
 
 
 def comparisons(ctx, L, u, f, y, n_owned, tmax):
-    """Comparison operators on the same workload (a11/a12): element-wise
+    """Per-operation rates on the same workload: surrogate
+    residual and GS sweep alone; comparison operators (a11/a12): element-wise
     on-the-fly FEM apply and constant-stencil (affine) apply, GLUP/s."""
     import torch
     res = {}
+    r = torch.empty_like(y)
+    uu = u.clone()
+    for name, fn, reps in (("surrogate_residual", lambda: ctx.residual(L, u, f, r), 5),
+                           ("surrogate_gs_sweep", lambda: ctx.gs_sweep(L, uu, f, 1), 5)):
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = tmax(e0.elapsed_time(e1) / reps)
+        res[name] = {"ms": ms, "glups": n_owned / (ms * 1e-3) / 1e9}
+    del r, uu
     for op, reps in (("surrogate", 5), ("const", 5), ("fem", 2)):
         ctx.apply(L, u, y, op=op)
         torch.cuda.synchronize()
@@ -421,8 +459,11 @@ def comparisons(ctx, L, u, f, y, n_owned, tmax):
 def other_configs(stream, q):
     """BASELINE configs 2 and 3 as context lines (1 GPU): config 2 = the single
     curved tet at L = 7 (333,375 unknowns, 2.7 MB per vector: L2-resident and
-    launch-bound, reported as-is), apply + 1 GS sweep per step; config 3 = the
-    480-macro shell at L = 6 (20.8 M unknowns), residual + 2 GS sweeps per step."""
+    launch-bound, reported as-is), apply + 1 GS sweep per step, and the same
+    tet as a batch of 480 copies (160 M unknowns: the roofline-
+    relevant single-tet number; every face Dirichlet, so volume kernels only);
+    config 3 = the 480-macro shell at L = 6 (20.8 M unknowns), residual + 2 GS
+    sweeps per step."""
     import numpy as np
     import torch
 
@@ -430,6 +471,7 @@ def other_configs(stream, q):
     import synth
     res = {}
     for name, mesh, L, kind in (("config2_single_tet_L7", synth.single_tet(), 7, "apply+gs"),
+                                ("config2_tet_batch480_L7", synth.tet_batch(480), 7, "apply+gs"),
                                 ("config3_shell480_L6", synth.shell_mesh(0.55, 1.0, 1, 2), 6, "resid+2gs")):
         ctx = hhg.Ctx.from_mesh(mesh, L, stream=stream.cuda_stream)
         ctx.fit(q, "lsqp", 2)
@@ -488,6 +530,68 @@ def cpu_baseline_parallel(step, n_unk, sample, seconds=8.0):
     value = sum(2 * n_unk * n / t for n, t in res) / 1e9
     return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": sample + f", one process per core, {seconds:.0f} s each"}
+
+
+def step_parity(ctx, mesh, L, q, u, f, y, step):
+    """Part of the oracle leg: one more bench step (apply + GS sweep) from a
+    snapshot u0, and at sampled volume nodes of a few macros the oracle's own
+    values (its LSQP fit of the node's macro; the GS update
+    replayed on the node's dependency cone of interior volume nodes, DESIGN.md
+    R13/R14): max |gpu - oracle| / (row magnitude)."""
+    import numpy as np
+    import torch
+    try:
+        from oracle import geometry as G, surrogate as S
+        N = 2 ** L
+        u0 = u.clone()
+        step()
+        torch.cuda.synchronize()
+        num = G.Numbering(mesh, N)
+        ug0, yg, ug1 = (np.asarray(ctx.gather_global(L, v)) for v in (u0, y, u))
+        fg = np.asarray(ctx.gather_global(L, f))
+        dirs = np.array(G.DIRS)
+        rng = np.random.default_rng(2024)
+        err_y, err_u, n = 0.0, 0.0, 0
+        for T in rng.choice(mesh.nt, 3, replace=False):
+            T = int(T)
+            a_T = S.fit_macro(mesh, T, L, q, "lsqp", 2, blended=True)
+            for _ in range(6):
+                while True:
+                    i, j, k = (int(x) for x in rng.integers(5, N - 5, 3))
+                    if i + j + k <= N - 5:
+                        break
+                ijk = np.array([[i, j, k]])
+                sw = S.eval_weights(a_T, ijk, N, q)[0]
+                gI = int(num.gids(T, ijk)[0])
+                un = ug0[num.gids(T, ijk + dirs)]
+                err_y = max(err_y, abs(yg[gI] - float(np.dot(sw, un))) / float(np.abs(sw * un).sum()))
+                memo = {}
+
+                def new_value(p):
+                    if p in memo:
+                        return memo[p]
+                    c = (p[0] + 2 * p[1] + 3 * p[2]) % 4
+                    pp = np.array([p])
+                    s2 = S.eval_weights(a_T, pp, N, q)[0]
+                    acc = mag = 0.0
+                    for w in range(15):
+                        if w == 7:
+                            continue
+                        qn = (p[0] + dirs[w][0], p[1] + dirs[w][1], p[2] + dirs[w][2])
+                        c2 = (qn[0] + 2 * qn[1] + 3 * qn[2]) % 4
+                        v = new_value(qn)[0] if c2 < c else ug0[int(num.gids(T, np.array([qn]))[0])]
+                        acc += s2[w] * v
+                        mag += abs(s2[w] * v)
+                    g = int(num.gids(T, pp)[0])
+                    memo[p] = ((fg[g] - acc) / s2[7], (abs(fg[g]) + mag) / abs(s2[7]))
+                    return memo[p]
+                ref, scale = new_value((i, j, k))
+                err_u = max(err_u, abs(ug1[gI] - ref) / scale)
+                n += 1
+        return {"nodes": n, "macros": 3, "apply_max_rel_err": err_y, "gs_max_rel_err": err_u,
+                "tolerance": 1e-12, "how": "sampled volume nodes >= 5 steps from their macro boundary"}
+    except Exception as e:  # pragma: no cover
+        return {"failed": str(e)}
 
 
 def cpu_baseline(L, q):

@@ -87,30 +87,26 @@ hhg_status face_centre_check(Ctx* c, Level& lv, int* d_flag) {
   return HHG_OK;
 }
 
-// Operands of a face row in summation order: un[e] = u at neighbour e
-// (entries 1..6 in-face, then the 4 into-macro entries of the macro with the
-// LOWER global id, then the other 4; 0 where a neighbour is absent), wv[e] the
-// matching weights (wv[0] = centre).  The canonical order makes the row's
-// rounding independent of which macro is local where (bitwise-equal results on
-// any number of ranks).
+// Summation order of a face row: centre, in-face entries 1..6, then the 4
+// into-macro entries of the macro with the LOWER global id, then the other 4
+// (F.bfirst: macro B's entries 11..14 first).  Canonical, so the row's
+// rounding is independent of which macro is local where (bitwise-equal
+// results on any number of ranks).  acc = fma(sgn * w_e, un_e, acc) in that order.
 template <class W>
-__device__ __forceinline__ void face_row_operands(const FaceLP& F, const FaceRowSlots& o,
-                                                  const double* __restrict__ u, W wgt, double (&un)[14],
-                                                  double (&wv)[15]) {
+__device__ __forceinline__ double face_row_chain(const FaceLP& F, double acc, double sgn, W w,
+                                                 const double (&un)[14]) {
 #pragma unroll
-  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
-#pragma unroll
-  for (int e = 0; e < 15; ++e) wv[e] = (e == 0 || o.nb[e - 1] >= 0) ? wgt(e) : 0.0;
+  for (int e = 0; e < 6; ++e) acc = fma(sgn * w(e + 1), un[e], acc);
   if (F.bfirst) {
 #pragma unroll
-    for (int e = 6; e < 10; ++e) {
-      const double a = un[e], w = wv[e + 1];
-      un[e] = un[e + 4];
-      wv[e + 1] = wv[e + 5];
-      un[e + 4] = a;
-      wv[e + 5] = w;
-    }
+    for (int e = 10; e < 14; ++e) acc = fma(sgn * w(e + 1), un[e], acc);
+#pragma unroll
+    for (int e = 6; e < 10; ++e) acc = fma(sgn * w(e + 1), un[e], acc);
+  } else {
+#pragma unroll
+    for (int e = 6; e < 14; ++e) acc = fma(sgn * w(e + 1), un[e], acc);
   }
+  return acc;
 }
 
 // mode: kModeApply / kModeResid (vol_kernels.cuh values 0 / 1)
@@ -132,13 +128,20 @@ __global__ void k_face_apply(int N, int64_t S, int64_t nfi, int64_t n_frows, con
   auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
     return fcoef ? face_poly(fcoef + (fc * 15 + e) * nfc, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
   };
-  // every gather and weight first (memory-level parallelism: the face rows
-  // are latency-bound, ncu r01h: long-scoreboard 74 %), then the fma chain
-  double un[14], wv[15];
-  face_row_operands(F, o, u, wgt, un, wv);
-  double acc = wv[0] * u[o.cA];
+  double un[14];
 #pragma unroll
-  for (int e = 0; e < 14; ++e) acc = fma(wv[e + 1], un[e], acc);
+  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
+  double acc;
+  if (fcoef) {  // all neighbour values first (memory-level parallelism), then the weights
+    acc = face_row_chain(F, wgt(0) * u[o.cA], 1.0, wgt, un);
+  } else {
+    // every gather and weight load first (memory-level parallelism: the face
+    // rows are latency-bound, ncu r01h: long-scoreboard 74 %), then the chain
+    double wv[15];
+#pragma unroll
+    for (int e = 0; e < 15; ++e) wv[e] = (e == 0 || o.nb[e - 1] >= 0) ? val[e * n_frows + r] : 0.0;
+    acc = face_row_chain(F, wv[0] * u[o.cA], 1.0, [&](int e) { return wv[e]; }, un);
+  }
   const double res = mode == 1 ? f[o.cA] - acc : acc;
   out[o.cA] = res;
   if (o.cB >= 0) out[o.cB] = res;
@@ -175,12 +178,18 @@ __global__ void k_face_gs(int N, int64_t S, int64_t nfi, int64_t nfc, int q0, co
   auto wgt = [&](int e) -> double {  // stored exact weight, or the face surrogate
     return fcoef ? face_poly(fcoef + (fc * 15 + e) * ncf, fq, st & 0xffff, st >> 16) : val[e * n_frows + r];
   };
-  double un[14], wv[15];
-  face_row_operands(F, o, u, wgt, un, wv);
-  double acc = f[o.cA];
+  double un[14];
 #pragma unroll
-  for (int e = 0; e < 14; ++e) acc = fma(-wv[e + 1], un[e], acc);
-  const double v = acc / wv[0];
+  for (int e = 0; e < 14; ++e) un[e] = o.nb[e] >= 0 ? u[o.nb[e]] : 0.0;
+  double v;
+  if (fcoef) {  // all neighbour values first (memory-level parallelism), then the weights
+    v = face_row_chain(F, f[o.cA], -1.0, wgt, un) / wgt(0);
+  } else {
+    double wv[15];
+#pragma unroll
+    for (int e = 0; e < 15; ++e) wv[e] = (e == 0 || o.nb[e - 1] >= 0) ? val[e * n_frows + r] : 0.0;
+    v = face_row_chain(F, f[o.cA], -1.0, [&](int e) { return wv[e]; }, un) / wv[0];
+  }
   if (face_inner(N, st & 0xffff, st >> 16)) {
     u[o.cA] = v;
     if (o.cB >= 0) u[o.cB] = v;

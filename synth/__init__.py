@@ -168,3 +168,15 @@ def single_tet(r1: float = 0.55, r2: float = 1.0) -> MacroMesh:
     tets = np.array([[0, 1, 2, 3]], dtype=np.int64)
     dirichlet = np.ones((1, 4), dtype=np.uint8)
     return MacroMesh(verts, rad, tets, dirichlet, name="single_tet")
+
+
+def tet_batch(n: int, r1: float = 0.55, r2: float = 1.0) -> MacroMesh:
+    """n disjoint copies of `single_tet` (BASELINE config 2 as a batch: the
+    same curved macro n times, every face Dirichlet, no shared primitives)."""
+    one = single_tet(r1, r2)
+    verts = np.tile(one.vertices, (n, 1))
+    rad = np.tile(one.radius, n)
+    tets = (np.arange(n, dtype=np.int64)[:, None] * 4 + np.arange(4, dtype=np.int64)[None, :])
+    dirichlet = np.ones((n, 4), dtype=np.uint8)
+    return MacroMesh(verts, rad, tets, dirichlet, name=f"tet_batch{n}")
+
