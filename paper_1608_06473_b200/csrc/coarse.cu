@@ -251,7 +251,7 @@ hhg_status coarse_build(Ctx* c, Level& lv) {
     const int nr = c->nranks;
     std::vector<int64_t> cnt_send(nr, (int64_t)cnt), cnt_recv(nr, 0);
     std::vector<int64_t> b8(nr, 8);
-    hhg_status st = dist_exchange_bytes(c, b8, cnt_send.data(), b8, cnt_recv.data(), false);
+    hhg_status st = dist_exchange_bytes(c, b8, cnt_send.data(), b8, cnt_recv.data(), false, c->stream);
     if (st != HHG_OK) return st;
     std::vector<int64_t> sb(nr), rb(nr);
     int64_t tot = 0;
@@ -262,7 +262,7 @@ hhg_status coarse_build(Ctx* c, Level& lv) {
     }
     std::vector<CooEntry> sendv((size_t)cnt * (nr - 1)), recvv((size_t)tot);
     for (int q = 0; q < nr - 1; ++q) std::copy(coo.begin(), coo.end(), sendv.begin() + (size_t)q * cnt);
-    st = dist_exchange_bytes(c, sb, sendv.data(), rb, recvv.data(), false);
+    st = dist_exchange_bytes(c, sb, sendv.data(), rb, recvv.data(), false, c->stream);
     if (st != HHG_OK) return st;
     coo.insert(coo.end(), recvv.begin(), recvv.end());
   }

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <functional>
 #include <cstring>
 #include <thread>
 
@@ -89,6 +90,10 @@ hhg_status ctx_sync(Ctx* c) {
 }
 
 void dist_destroy(Ctx* c) {
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  c->comm_stream = nullptr;
   if (c->nccl_comm) ncclCommDestroy((ncclComm_t)c->nccl_comm);
   c->nccl_comm = nullptr;
   if (c->h_stage) cudaFreeHost(c->h_stage);
@@ -97,7 +102,8 @@ void dist_destroy(Ctx* c) {
 
 // Pairwise exchange of byte ranges (buffers concatenated in rank order).
 hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& sb, const void* send,
-                               const std::vector<int64_t>& rb, void* recv, bool device) {
+                               const std::vector<int64_t>& rb, void* recv, bool device, cudaStream_t stream) {
+  if (!stream) stream = c->stream;
   const int nr = c->nranks;
   int64_t ts = 0, tr = 0;
   for (int p = 0; p < nr; ++p) ts += sb[p], tr += rb[p];
@@ -109,21 +115,21 @@ hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& sb, const voi
       HHG_CK(c, cudaMalloc(&ds, std::max<int64_t>(ts, 1)));
       HHG_CK(c, cudaMalloc(&dr, std::max<int64_t>(tr, 1)));
       // stream-ordered before the sends (the ctx stream may be a non-blocking stream)
-      HHG_CK(c, cudaMemcpyAsync(ds, send, ts, cudaMemcpyHostToDevice, c->stream));
+      HHG_CK(c, cudaMemcpyAsync(ds, send, ts, cudaMemcpyHostToDevice, stream));
       s = (const char*)ds;
       r = (char*)dr;
     }
     HHG_NCCL(c, ncclGroupStart());
     int64_t so = 0, ro = 0;
     for (int p = 0; p < nr; ++p) {
-      if (sb[p]) HHG_NCCL(c, ncclSend(s + so, sb[p], ncclChar, p, (ncclComm_t)c->nccl_comm, c->stream));
-      if (rb[p]) HHG_NCCL(c, ncclRecv(r + ro, rb[p], ncclChar, p, (ncclComm_t)c->nccl_comm, c->stream));
+      if (sb[p]) HHG_NCCL(c, ncclSend(s + so, sb[p], ncclChar, p, (ncclComm_t)c->nccl_comm, stream));
+      if (rb[p]) HHG_NCCL(c, ncclRecv(r + ro, rb[p], ncclChar, p, (ncclComm_t)c->nccl_comm, stream));
       so += sb[p];
       ro += rb[p];
     }
     HHG_NCCL(c, ncclGroupEnd());
     if (!device) {
-      HHG_CK(c, cudaMemcpyAsync(recv, dr, tr, cudaMemcpyDeviceToHost, c->stream));
+      HHG_CK(c, cudaMemcpyAsync(recv, dr, tr, cudaMemcpyDeviceToHost, stream));
       { hhg_status st_sync__ = ctx_sync(c); if (st_sync__ != HHG_OK) return st_sync__; }
       cudaFree(ds);
       cudaFree(dr);
@@ -145,11 +151,13 @@ hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& sb, const voi
     }
     char* hs = (char*)c->h_stage;
     char* hr = hs + ts;
-    HHG_CK(c, cudaMemcpyAsync(hs, send, ts, cudaMemcpyDeviceToHost, c->stream));
-    HHG_CK(c, cudaStreamSynchronize(c->stream));
+    HHG_CK(c, cudaMemcpyAsync(hs, send, ts, cudaMemcpyDeviceToHost, stream));
+    HHG_CK(c, cudaStreamSynchronize(stream));
     if (fn(c->host_user, nr, sb.data(), hs, rb.data(), hr) != 0)
       return set_err(c, HHG_ERR_NCCL, "host transport failed");
-    HHG_CK(c, cudaMemcpyAsync(recv, hr, tr, cudaMemcpyHostToDevice, c->stream));
+    HHG_CK(c, cudaMemcpyAsync(recv, hr, tr, cudaMemcpyHostToDevice, stream));
+    // the staging buffer is reused by the next exchange, possibly on another stream
+    HHG_CK(c, cudaStreamSynchronize(stream));
     return HHG_OK;
   }
   return set_err(c, HHG_ERR_STATE, "no transport");
@@ -177,7 +185,7 @@ hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_
   // counts: I tell every peer how many values I need from it
   std::vector<int64_t> one(nr, (int64_t)sizeof(int64_t));
   std::vector<int64_t> cnt_recv(nr, 0);
-  hhg_status st = dist_exchange_bytes(c, one, lv.recv_cnt.data(), one, cnt_recv.data(), false);
+  hhg_status st = dist_exchange_bytes(c, one, lv.recv_cnt.data(), one, cnt_recv.data(), false, c->stream);
   if (st != HHG_OK) return st;
   lv.send_cnt = cnt_recv;
   std::vector<int64_t> sb(nr), rb(nr);
@@ -188,7 +196,7 @@ hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_
     nsend += lv.send_cnt[p];
   }
   std::vector<int64_t> asked(nsend);
-  st = dist_exchange_bytes(c, sb, lv.h_recv_gid.data(), rb, asked.data(), false);
+  st = dist_exchange_bytes(c, sb, lv.h_recv_gid.data(), rb, asked.data(), false, c->stream);
   if (st != HHG_OK) return st;
   // resolve requested ids to this rank's authoritative slots
   std::vector<std::array<int, 3>> vinv(g.nvi);
@@ -264,11 +272,12 @@ __global__ void k_unpack(int64_t n, const uint32_t* __restrict__ slot, const dou
   if (t < n) v[slot[t]] = buf[t];
 }
 
-hhg_status dist_sync(Ctx* c, Level& lv, double* v) {
+hhg_status dist_sync(Ctx* c, Level& lv, double* v, cudaStream_t stream) {
   if (c->nranks == 1) return HHG_OK;
+  if (!stream) stream = c->stream;
   ProfScope ps(c, 3);
   if (lv.n_send) {
-    k_pack<<<(unsigned)((lv.n_send + 255) / 256), 256, 0, c->stream>>>(lv.n_send, lv.d_send_slot, v, lv.d_sendbuf);
+    k_pack<<<(unsigned)((lv.n_send + 255) / 256), 256, 0, stream>>>(lv.n_send, lv.d_send_slot, v, lv.d_sendbuf);
     HHG_LAUNCHED(c);
   }
   std::vector<int64_t> sb(c->nranks), rb(c->nranks);
@@ -276,12 +285,36 @@ hhg_status dist_sync(Ctx* c, Level& lv, double* v) {
     sb[p] = lv.send_cnt[p] * 8;
     rb[p] = lv.recv_cnt[p] * 8;
   }
-  hhg_status st = dist_exchange_bytes(c, sb, lv.d_sendbuf, rb, lv.d_recvbuf, true);
+  hhg_status st = dist_exchange_bytes(c, sb, lv.d_sendbuf, rb, lv.d_recvbuf, true, stream);
   if (st != HHG_OK) return st;
   if (lv.n_recv) {
-    k_unpack<<<(unsigned)((lv.n_recv + 255) / 256), 256, 0, c->stream>>>(lv.n_recv, lv.d_recv_slot, lv.d_recvbuf, v);
+    k_unpack<<<(unsigned)((lv.n_recv + 255) / 256), 256, 0, stream>>>(lv.n_recv, lv.d_recv_slot, lv.d_recvbuf, v);
     HHG_LAUNCHED(c);
   }
+  return HHG_OK;
+}
+
+// Ghost exchange of v overlapped with compute: the exchange runs
+// on the ctx's communication stream after everything enqueued so far on the
+// ctx stream (the values it sends are final), while `interior` -- work that
+// neither writes a sent value nor reads / writes a received slot -- is
+// enqueued on the ctx stream; the ctx stream then waits for the exchange.
+hhg_status dist_sync_overlapped(Ctx* c, Level& lv, double* v, const std::function<hhg_status()>& interior) {
+  if (c->nranks == 1) return interior();
+  if (!c->comm_stream) {
+    HHG_CK(c, cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    HHG_CK(c, cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    HHG_CK(c, cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  }
+  HHG_CK(c, cudaEventRecord(c->ev_fork, c->stream));
+  HHG_CK(c, cudaStreamWaitEvent(c->comm_stream, c->ev_fork, 0));
+  // the interior work is enqueued first: with the host transport the exchange
+  // blocks this thread, and the GPU must already have the interior kernels
+  hhg_status st = interior();
+  if (st != HHG_OK) return st;
+  if ((st = dist_sync(c, lv, v, c->comm_stream)) != HHG_OK) return st;
+  HHG_CK(c, cudaEventRecord(c->ev_join, c->comm_stream));
+  HHG_CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
   return HHG_OK;
 }
 
@@ -312,7 +345,7 @@ hhg_status dist_sum_to_owner(Ctx* c, Level& lv, double* v) {
     sb[p] = lv.recv_cnt[p] * 8;
     rb[p] = lv.send_cnt[p] * 8;
   }
-  hhg_status st = dist_exchange_bytes(c, sb, lv.d_recvbuf, rb, lv.d_sendbuf, true);
+  hhg_status st = dist_exchange_bytes(c, sb, lv.d_recvbuf, rb, lv.d_sendbuf, true, c->stream);
   if (st != HHG_OK) return st;
   if (lv.n_rsum) {
     k_unpack_sum<<<(unsigned)((lv.n_rsum + 255) / 256), 256, 0, c->stream>>>(lv.n_rsum, lv.d_rsum_ptr, lv.d_rsum_slot,
@@ -351,7 +384,7 @@ hhg_status dist_allreduce_sum(Ctx* c, double* d_scalar) {
     double* sendv = buf;                 // nr entries, self entry unused (0 bytes)
     double* recvv = nullptr;
     HHG_CK(c, cudaMallocAsync((void**)&recvv, nr * sizeof(double), c->stream));
-    hhg_status st = dist_exchange_bytes(c, sbc, sendv, rbc, recvv, true);
+    hhg_status st = dist_exchange_bytes(c, sbc, sendv, rbc, recvv, true, c->stream);
     if (st != HHG_OK) return st;
     // recvv holds the peers' values in rank order (self skipped): scatter into buf[nr..]
     int q = 0;
@@ -397,7 +430,7 @@ hhg_status dist_allreduce_vec(Ctx* c, double* d_vec, int64_t n) {
   std::vector<int64_t> sb(nr, n * 8), rb(nr, n * 8);
   sb[c->rank] = 0;
   rb[c->rank] = 0;
-  hhg_status st = dist_exchange_bytes(c, sb, sendv, rb, recvv, true);
+  hhg_status st = dist_exchange_bytes(c, sb, sendv, rb, recvv, true, c->stream);
   if (st != HHG_OK) return st;
   k_sum_vec_ranks<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(nr, c->rank, n, recvv, d_vec);
   HHG_LAUNCHED(c);
@@ -454,7 +487,7 @@ extern "C" hhg_status hhg_plan_check(hhg_ctx ctx, int L, int64_t* mismatches) {
     rb[p] = lv.recv_cnt[p] * 8;
   }
   std::vector<int64_t> got(lv.n_recv);
-  hhg_status st = dist_exchange_bytes(c, sb, lv.h_send_gid.data(), rb, got.data(), false);
+  hhg_status st = dist_exchange_bytes(c, sb, lv.h_send_gid.data(), rb, got.data(), false, c->stream);
   if (st != HHG_OK) return st;
   int64_t bad = 0;
   for (int64_t x = 0; x < lv.n_recv; ++x) bad += got[x] != lv.h_recv_gid[x];

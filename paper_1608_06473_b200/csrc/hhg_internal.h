@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <functional>
 #include <map>
 #include <set>
 #include <string>
@@ -232,6 +233,9 @@ struct Ctx {
   bool poisoned = false;
   cudaStream_t stream = nullptr;
   cudaStream_t cap_stream = nullptr;  // graph capture (the ctx stream may be the legacy default stream)
+  cudaStream_t comm_stream = nullptr; // ghost exchange overlapped with interior macros (dist.cu)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int64_t nt_bnd = 0;                 // local macros [0, nt_bnd) touch another rank's macros (boundary)
   // cached V-cycle graph (hhg_vcycle): replayed while the call signature matches
   cudaGraphExec_t vc_graph = nullptr;
   int64_t vc_graph_launches = 0;
@@ -338,11 +342,13 @@ hhg_status dist_init_transport(Ctx* c, const void* nccl_unique_id);
 void dist_destroy(Ctx* c);
 hhg_status ctx_sync(Ctx* c);
 hhg_status dist_exchange_bytes(Ctx* c, const std::vector<int64_t>& send_bytes, const void* send,
-                               const std::vector<int64_t>& recv_bytes, void* recv, bool device);
+                               const std::vector<int64_t>& recv_bytes, void* recv, bool device,
+                               cudaStream_t stream);
 hhg_status dist_build_plan(Ctx* c, Level& lv, const std::vector<uint32_t>& recv_slot,
                            const std::vector<int64_t>& recv_gid, const std::vector<int32_t>& recv_rank,
                            const std::vector<std::pair<int64_t, uint32_t>>& serve);
-hhg_status dist_sync(Ctx* c, Level& lv, double* v);
+hhg_status dist_sync(Ctx* c, Level& lv, double* v, cudaStream_t stream = nullptr);
+hhg_status dist_sync_overlapped(Ctx* c, Level& lv, double* v, const std::function<hhg_status()>& interior);
 hhg_status dist_sum_to_owner(Ctx* c, Level& lv, double* v);
 hhg_status dist_allreduce_sum(Ctx* c, double* d_scalar);
 

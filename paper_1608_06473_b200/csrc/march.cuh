@@ -553,11 +553,12 @@ template <int OP>
 __global__ void __launch_bounds__(kMarchThreads, 2)
     k_gs_march(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, int colour,
-               double* __restrict__ u, const double* __restrict__ f) {
+               double* __restrict__ u, const double* __restrict__ f, int64_t T0) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem<> sm(smem, slot_len);
-  const int64_t T = blockIdx.x / n_bands;
-  const Band b = bands[blockIdx.x - T * n_bands];
+  const int64_t Tr = blockIdx.x / n_bands;
+  const int64_t T = T0 + Tr;
+  const Band b = bands[blockIdx.x - Tr * n_bands];
   Column q;
   double A[15], B[15];
   band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
@@ -582,8 +583,8 @@ template <int OP, int NT, int RING>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
-               const double* __restrict__ f, int64_t ntl, int* __restrict__ counter, int* __restrict__ flags,
-               int epoch, int stress) {
+               const double* __restrict__ f, int64_t ntl, int64_t T0, int* __restrict__ counter,
+               int* __restrict__ flags, int epoch, int stress) {
   extern __shared__ __align__(16) double smem[];
   MarchSmem<RING> sm(smem, slot_len);
   __shared__ int s_item;
@@ -597,10 +598,11 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const int64_t item = s_item;
     __syncthreads();
     if (item >= total) break;
-    const int64_t T = item / n_bands;
+    const int64_t Tr = item / n_bands;  // macro within the launch's range [T0, T0 + ntl)
+    const int64_t T = T0 + Tr;
     // stress test (HHG_GS_STRESS): bands of a macro handed out in reverse order
     // (macro-major order kept: still deadlock-free) and random delays below
-    const int band = (stress & 1) ? n_bands - 1 - (int)(item - T * n_bands) : (int)(item - T * n_bands);
+    const int band = (stress & 1) ? n_bands - 1 - (int)(item - Tr * n_bands) : (int)(item - Tr * n_bands);
     const double* const Cw = sm.Cw;
     const Band b = bands[band];
     Column q;

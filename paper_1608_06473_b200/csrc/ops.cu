@@ -292,15 +292,16 @@ static hhg_status resident_grid(Ctx* c, const void* fn, int threads, size_t smem
 }
 
 template <int OP, int MODE>
-static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double* f, double* out) {
+static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double* f, double* out, int64_t Tb,
+                               int64_t Te) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
   hhg_status st = smem_attr(c, (const void*)k_vol_march<OP, MODE>);
   if (st != HHG_OK) return st;
   const int nb = (int)lv.bands.size();
   if ((st = ensure_cC(c, lv, OP)) != HHG_OK) return st;
   ProfScope ps(c, 0);
-  for (int64_t T0 = 0; T0 < c->nt_local; T0 += kCMax) {
-    const int64_t nt = std::min<int64_t>(kCMax, c->nt_local - T0);
+  for (int64_t T0 = Tb; T0 < Te; T0 += kCMax) {
+    const int64_t nt = std::min<int64_t>(kCMax, Te - T0);
     if (OP == HHG_OP_SURROGATE)
       HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, nt * 15 * sizeof(double), 0,
                                         cudaMemcpyDeviceToDevice, c->stream));
@@ -313,16 +314,24 @@ static hhg_status launch_march(Ctx* c, Level& lv, const double* u, const double*
 
 // One GS colour pass over every band (the fallback of the persistent sweep).
 template <int OP>
-static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, const double* f) {
+static hhg_status launch_gs_march(Ctx* c, Level& lv, int colour, double* u, const double* f, int64_t Tb,
+                                  int64_t Te) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N);
   hhg_status st = smem_attr(c, (const void*)k_gs_march<OP>);
   if (st != HHG_OK) return st;
   const int nb = (int)lv.bands.size();
   ProfScope ps(c, 1);
-  k_gs_march<OP><<<(unsigned)(nb * c->nt_local), kMarchThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, colour, u, f);
+  if (Te <= Tb) return HHG_OK;
+  k_gs_march<OP><<<(unsigned)(nb * (Te - Tb)), kMarchThreads, smem, c->stream>>>(
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, colour, u, f, Tb);
   HHG_LAUNCHED(c);
   return HHG_OK;
+}
+
+// HHG_OVERLAP=0 (read per call): no exchange / interior-compute overlap on multi-rank
+static bool overlap_on() {
+  const char* e = getenv("HHG_OVERLAP");
+  return !(e && atoi(e) == 0);
 }
 
 // HHG_GS_STRESS=<seed> (tests): the persistent GS kernels hand out the bands of
@@ -334,7 +343,7 @@ static int gs_stress() {
 
 // The whole volume GS (4 colours) as one persistent launch (march.cuh::k_gs_items).
 template <int OP, int RING>
-static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* f) {
+static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* f, int64_t Tb, int64_t Te) {
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N, RING);
   const void* fn = (const void*)k_gs_items<OP, kMarchThreads, RING>;
   hhg_status st = smem_attr(c, fn);
@@ -348,23 +357,25 @@ static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* 
   if (grid <= nb) return HHG_ERR_STATE;
   // completion flags cleared per sweep (epoch 1): the launch is replayable from
   // a CUDA graph (hhg_vcycle)
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags, 0, (size_t)c->nt_local * nb * 4 * sizeof(int), c->stream));
+  const int64_t ntr = Te - Tb;
+  if (ntr <= 0) return HHG_OK;
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags + Tb * nb * 4, 0, (size_t)ntr * nb * 4 * sizeof(int), c->stream));
   lv.gs_epoch = 1;
   HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
-  const int64_t items = c->nt_local * nb;
+  const int64_t items = ntr * nb;
   ProfScope ps(c, 1);
   k_gs_items<OP, kMarchThreads, RING><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, c->nt_local, lv.d_gs_counter,
+      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, ntr, Tb, lv.d_gs_counter,
       lv.d_gs_flags, lv.gs_epoch, gs_stress());
   HHG_LAUNCHED(c);
   return HHG_OK;
 }
 
 template <int OP>
-static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f) {
+static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f, int64_t Tb, int64_t Te) {
   // 24-plane ring only while two CTAs fit an SM (N = 256: 768-double slots -> 16)
-  if (march_smem_bytes(lv.slot_len, lv.N, 24) > 113 * 1024) return launch_gs_items_r<OP, 16>(c, lv, u, f);
-  return launch_gs_items_r<OP, 24>(c, lv, u, f);
+  if (march_smem_bytes(lv.slot_len, lv.N, 24) > 113 * 1024) return launch_gs_items_r<OP, 16>(c, lv, u, f, Tb, Te);
+  return launch_gs_items_r<OP, 24>(c, lv, u, f, Tb, Te);
 }
 
 // The whole volume GS (4 colours) as one single-pass wavefront launch
@@ -422,20 +433,29 @@ static hhg_status launch_gs_front(Ctx* c, Level& lv, double* u, const double* f,
   }
 }
 
+// Whether the volume pass of (op, mode) runs the column-march kernels, which
+// take a macro range (the overlapped exchange splits boundary / interior macros).
+static bool march_path(const Level& lv, int op) {
+  if (op == HHG_OP_SURROGATE_FACES) op = HHG_OP_SURROGATE;
+  return !lv.bands.empty() && ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
+}
+
 static hhg_status volume_pass(Ctx* c, Level& lv, int op, int mode, int colour, const double* u,
-                              const double* f, double* out) {
+                              const double* f, double* out, int64_t Tb = 0, int64_t Te = -1) {
+  if (Te < 0) Te = c->nt_local;
   if (op == HHG_OP_SURROGATE_FACES) op = HHG_OP_SURROGATE;  // volume rows: the surrogate
   // column-march kernels: q <= 2 surrogate (s_w quadratic along a column) and the constant stencil
-  const bool march = !lv.bands.empty() && ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
+  const bool march = march_path(lv, op);
+  if (!march && (Tb != 0 || Te != c->nt_local)) return set_err(c, HHG_ERR_STATE, "macro range on a full-grid kernel");
   if (march && mode == kModeGS)
-    return op == HHG_OP_SURROGATE ? launch_gs_march<HHG_OP_SURROGATE>(c, lv, colour, out, f)
-                                  : launch_gs_march<HHG_OP_CONST_AFFINE>(c, lv, colour, out, f);
+    return op == HHG_OP_SURROGATE ? launch_gs_march<HHG_OP_SURROGATE>(c, lv, colour, out, f, Tb, Te)
+                                  : launch_gs_march<HHG_OP_CONST_AFFINE>(c, lv, colour, out, f, Tb, Te);
   if (march) {
     if (op == HHG_OP_SURROGATE)
-      return mode == kModeApply ? launch_march<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out)
-                                : launch_march<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out);
-    return mode == kModeApply ? launch_march<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out)
-                              : launch_march<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out);
+      return mode == kModeApply ? launch_march<HHG_OP_SURROGATE, kModeApply>(c, lv, u, f, out, Tb, Te)
+                                : launch_march<HHG_OP_SURROGATE, kModeResid>(c, lv, u, f, out, Tb, Te);
+    return mode == kModeApply ? launch_march<HHG_OP_CONST_AFFINE, kModeApply>(c, lv, u, f, out, Tb, Te)
+                              : launch_march<HHG_OP_CONST_AFFINE, kModeResid>(c, lv, u, f, out, Tb, Te);
   }
   if (op == HHG_OP_FEM_ELEMENTWISE && mode != kModeGS && !lv.bands.empty()) {
     // plane range per band (the first band's also holds diagonal 0)
@@ -620,26 +640,49 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
   const char* e = getenv("HHG_GS_KERNEL");
   const std::string ks = e ? e : "";
   const int mode = ks == "passes" ? 1 : ks == "front" ? 3 : ks == "front6" ? 4 : ks == "wide4" ? 5 : ks == "wide6" ? 6 : 2;
-  const bool march_ok = !lv.bands.empty() && ((op == HHG_OP_SURROGATE && lv.d_coef10) || op == HHG_OP_CONST_AFFINE);
-  hhg_status st = HHG_ERR_STATE;
-  if (march_ok && mode == 2)
-    st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f)
-                                : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f);
-  if (march_ok && mode >= 3) {
-    const int variant = mode - 3;
-    st = op == HHG_OP_SURROGATE ? launch_gs_front<HHG_OP_SURROGATE>(c, lv, u, f, variant)
-                                : launch_gs_front<HHG_OP_CONST_AFFINE>(c, lv, u, f, variant);
+  const bool march_ok = march_path(lv, op);
+  auto sweep = [&](int64_t Tb, int64_t Te) -> hhg_status {
+    hhg_status st = HHG_ERR_STATE;
+    if (march_ok && mode == 2)
+      st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f, Tb, Te)
+                                  : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f, Tb, Te);
+    if (march_ok && mode >= 3 && Tb == 0 && Te == c->nt_local) {
+      const int variant = mode - 3;
+      st = op == HHG_OP_SURROGATE ? launch_gs_front<HHG_OP_SURROGATE>(c, lv, u, f, variant)
+                                  : launch_gs_front<HHG_OP_CONST_AFFINE>(c, lv, u, f, variant);
+    }
+    if (st != HHG_OK) {
+      if (c->poisoned) return HHG_ERR_CUDA;
+      for (int col = 0; col < 4; ++col)
+        if ((st = volume_pass(c, lv, op, kModeGS, col, u, f, u, march_ok ? Tb : 0, march_ok ? Te : -1)) != HHG_OK)
+          return st;
+    }
+    return HHG_OK;
+  };
+  // multi-rank: the ghost exchange of the swept volume values overlaps the
+  // sweep of the interior macros (HHG_OVERLAP=0 disables)
+  if (c->nranks > 1 && march_ok && (mode == 1 || mode == 2) && overlap_on()) {
+    hhg_status st = sweep(0, c->nt_bnd);
+    if (st != HHG_OK) return st;
+    return dist_sync_overlapped(c, lv, u, [&]() { return sweep(c->nt_bnd, c->nt_local); });
   }
-  if (st != HHG_OK) {
-    if (c->poisoned) return HHG_ERR_CUDA;
-    for (int col = 0; col < 4; ++col)
-      if ((st = volume_pass(c, lv, op, kModeGS, col, u, f, u)) != HHG_OK) return st;
-  }
+  hhg_status st = sweep(0, c->nt_local);
+  if (st != HHG_OK) return st;
   return dist_sync(c, lv, u);  // ghost volume values for the other ranks
 }
 
 hhg_status apply_dev(Ctx* c, Level& lv, int op, int mode, const double* u, const double* f, double* y) {
   hhg_status st;
+  if (c->nranks > 1 && march_path(lv, op) && overlap_on()) {
+    // boundary macros and the lower-primitive rows first; the exchange of the
+    // rows' owner values and of the boundary volume values then overlaps the
+    // interior macros' volume pass (they send and receive nothing)
+    if ((st = volume_pass(c, lv, op, mode, 0, u, f, y, 0, c->nt_bnd)) != HHG_OK) return st;
+    if ((st = lp_pass(c, lv, op, mode, u, f, y)) != HHG_OK) return st;
+    st = dist_sync_overlapped(c, lv, y, [&]() { return volume_pass(c, lv, op, mode, 0, u, f, y, c->nt_bnd, c->nt_local); });
+    if (st != HHG_OK) return st;
+    return zero_dir(c, lv, y);
+  }
   if ((st = volume_pass(c, lv, op, mode, 0, u, f, y)) != HHG_OK) return st;
   if ((st = lp_pass(c, lv, op, mode, u, f, y)) != HHG_OK) return st;
   if ((st = dist_sync(c, lv, y)) != HHG_OK) return st;  // owners' rows -> every copy / ghost

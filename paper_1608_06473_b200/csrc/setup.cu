@@ -765,9 +765,23 @@ extern "C" hhg_status hhg_setup_macro_mesh(const double* vertices, const double*
   for (int64_t t = 0; t < nt; ++t)
     if (c->owner[t] == rank)
       for (int a = 0; a < 4; ++a) vlocal[gtopo[t].gv[a]] = 1;
-  c->local_macros.clear();
+  // local macros: BOUNDARY ones first (a vertex shared with another rank's
+  // macro: their values are exchanged), then the interior ones, each in
+  // ascending global id -- the exchange can then overlap the interior range
+  // (dist_sync_overlapped)
+  std::vector<char> vforeign(nv, 0);
   for (int64_t t = 0; t < nt; ++t)
-    if (c->owner[t] == rank) c->local_macros.push_back(t);
+    if (c->owner[t] != rank)
+      for (int a = 0; a < 4; ++a) vforeign[gtopo[t].gv[a]] = 1;
+  c->local_macros.clear();
+  for (int pass = 0; pass < 2; ++pass)
+    for (int64_t t = 0; t < nt; ++t) {
+      if (c->owner[t] != rank) continue;
+      bool b = false;
+      for (int a = 0; a < 4; ++a) b = b || vforeign[gtopo[t].gv[a]];
+      if (b == (pass == 0)) c->local_macros.push_back(t);
+      if (pass == 0 && b) ++c->nt_bnd;
+    }
   c->nt_local = (int64_t)c->local_macros.size();
   for (int64_t t = 0; t < nt; ++t) {
     if (c->owner[t] == rank) continue;
