@@ -264,6 +264,10 @@ constexpr int kCMax = 512;
 #define HHG_RESID_UNROLL 2
 #endif
 constexpr int kResidUnroll = HHG_RESID_UNROLL;
+#ifndef HHG_APPLY_UNROLL
+#define HHG_APPLY_UNROLL 1
+#endif
+constexpr int kApplyUnroll = HHG_APPLY_UNROLL;
 #ifndef HHG_GS_UNROLL
 #define HHG_GS_UNROLL 3
 #endif
@@ -313,7 +317,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 #pragma unroll
   for (int x = 0; x < FPD; ++x)
     fq[x] = (MODE == kModeResid && q.active && 1 + x <= q.len) ? __ldg(fptr + sm.po[1 + x]) : 0.0;
-#pragma unroll(MODE == kModeResid ? kResidUnroll : 1)
+#pragma unroll(MODE == kModeResid ? kResidUnroll : kApplyUnroll)
   for (int k = 1; k <= b.kmax; ++k) {
     const int po2 = sm.po[k + 1];
     const double fv = fq[0];
