@@ -173,16 +173,18 @@ struct MarchSmem {
   uint64_t* bars;   // [RING]
   double* Cw;       // [16] k^2 coefficients of the 15 weights (per macro)
   int* po;          // [N+2] plane offsets
-  __device__ MarchSmem(double* smem, int slot_len) {
+  int* roff;        // [N+2] ring offset of plane p for the current band (GS passes; set by band_setup)
+  __device__ MarchSmem(double* smem, int slot_len, int N = 0) {
     ring = smem;
     bars = (uint64_t*)(smem + RING * slot_len);
     Cw = (double*)(bars + RING);
     po = (int*)(Cw + 16);
+    roff = po + (N + 2);
   }
 };
 
 __host__ __device__ inline size_t march_smem_bytes(int slot_len, int N, int ring = kRing) {
-  return (size_t)ring * slot_len * 8 + ring * 8 + 16 * 8 + (size_t)(N + 2) * 4;
+  return (size_t)ring * slot_len * 8 + ring * 8 + 16 * 8 + (size_t)2 * (N + 2) * 4;
 }
 
 struct Column {
@@ -383,9 +385,7 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
   int next_issue = min(RING, last_plane + 1);
   issue_planes<RING>(ub, sm.po, 0, next_issue - 1, b, sm.ring, slot_len, sm.bars);
   const int clo = b.c_lo;
-  auto sptr = [&](int p) -> const double* {
-    return sm.ring + (p % RING) * slot_len + ((sm.po[p] + clo) & 1);
-  };
+  auto sptr = [&](int p) -> const double* { return sm.ring + sm.roff[p]; };
   auto wait_plane = [&](int p) {
     if (p <= last_plane) mbar_wait(&sm.bars[p % RING], (p / RING) & 1);
   };
@@ -473,9 +473,7 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
   };
   int next_quad = min(NQ, last_quad + 1);
   issue_quads(0, next_quad - 1);
-  auto sptr = [&](int p) -> const double* {
-    return sm.ring + (p % RING) * slot_len + ((sm.po[p] + clo) & 1);
-  };
+  auto sptr = [&](int p) -> const double* { return sm.ring + sm.roff[p]; };
   int waited = -1;
   auto wait_quads = [&](int qq) {
     qq = min(qq, last_quad);
@@ -542,13 +540,18 @@ __device__ __forceinline__ void gs_quad_bars_init(MarchSmem<RING>& sm) {
 }
 
 template <int OP, int RING = kRing>
-__device__ __forceinline__ void band_setup(MarchSmem<RING>& sm, int N, const Band& b, int64_t T,
+__device__ __forceinline__ void band_setup(MarchSmem<RING>& sm, int N, const Band& b, int64_t T, int slot_len,
                                            const double* __restrict__ coef10, const double* __restrict__ cons,
                                            Column& q, double (&A)[15], double (&B)[15]) {
   q = make_column(b, N);
   column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
   if (threadIdx.x < 15) sm.Cw[threadIdx.x] = (OP == HHG_OP_SURROGATE) ? coef10[T * 150 + threadIdx.x * 10 + 9] : 0.0;
-  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) sm.po[p] = (int)plane_off(N, p);
+  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) {
+    const int pof = (int)plane_off(N, p);
+    sm.po[p] = pof;
+    // ring slot of plane p + the 16-byte alignment shift of its bulk copy
+    sm.roff[p] = (p % RING) * slot_len + ((pof + b.c_lo) & 1);
+  }
   __syncthreads();
 }
 
@@ -559,13 +562,13 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
                const double* __restrict__ coef10, const double* __restrict__ cons, int colour,
                double* __restrict__ u, const double* __restrict__ f, int64_t T0) {
   extern __shared__ __align__(16) double smem[];
-  MarchSmem<> sm(smem, slot_len);
+  MarchSmem<> sm(smem, slot_len, N);
   const int64_t Tr = blockIdx.x / n_bands;
   const int64_t T = T0 + Tr;
   const Band b = bands[blockIdx.x - Tr * n_bands];
   Column q;
   double A[15], B[15];
-  band_setup<OP>(sm, N, b, T, coef10, cons, q, A, B);
+  band_setup<OP>(sm, N, b, T, slot_len, coef10, cons, q, A, B);
   gs_colour_pass<OP>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
 }
 
@@ -590,7 +593,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
                const double* __restrict__ f, int64_t ntl, int64_t T0, int* __restrict__ counter,
                int* __restrict__ flags, int epoch, int stress) {
   extern __shared__ __align__(16) double smem[];
-  MarchSmem<RING> sm(smem, slot_len);
+  MarchSmem<RING> sm(smem, slot_len, N);
   __shared__ int s_item;
   const int64_t total = ntl * n_bands;
 #ifdef HHG_GS_PROF
@@ -613,7 +616,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     double A[15], B[15];
     {
       GPROF_T0
-      band_setup<OP, RING>(sm, N, b, T, coef10, cons, q, A, B);
+      band_setup<OP, RING>(sm, N, b, T, slot_len, coef10, cons, q, A, B);
       GPROF_ADD(4)
     }
     constexpr bool kQuad = RING % 8 == 0 && RING >= 24;
