@@ -27,15 +27,6 @@
 
 namespace hhg {
 
-// Optional cycle accounting of the GS kernels (build with -DHHG_GS_PROF; tools/gsprof.py).
-#ifdef HHG_GS_PROF
-__device__ unsigned long long g_gsprof[12];
-#define GPROF_T0 long long _t0 = clock64();
-#define GPROF_ADD(i) if (threadIdx.x == 0) atomicAdd(&g_gsprof[i], (unsigned long long)(clock64() - _t0));
-#else
-#define GPROF_T0
-#define GPROF_ADD(i)
-#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -393,10 +384,8 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
   double f_next = 0.0;
   if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
   {
-    GPROF_T0
     wait_plane(0);
     wait_plane(1);
-    GPROF_ADD(2)
   }
   for (int s = 0; s < nsteps; ++s) {
     // planes 4s+1 .. 4s+4 become needed at step s (4s-1, 4s were waited before)
@@ -439,9 +428,6 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
                                                  double* __restrict__ wb, const double* __restrict__ Cw,
                                                  bool init_bars = true) {
   constexpr int NQ = RING / 4;
-#ifdef HHG_GS_PROF
-  long long _tp0 = clock64();
-#endif
   if (init_bars) {  // else the caller initialised them (gs_quad_bars_init) before a CTA barrier
     if (threadIdx.x == 0) {
       for (int s = 0; s < NQ; ++s) mbar_init(&sm.bars[s], 4);
@@ -485,17 +471,11 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
   const int nsteps = (b.kmax + 4) / 4;
   double f_next = 0.0;
   if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
-#ifdef HHG_GS_PROF
-  if (threadIdx.x == 0) atomicAdd(&g_gsprof[8], (unsigned long long)(clock64() - _tp0));
-#endif
 #pragma unroll(kGsUnroll)
   for (int s = 0; s < nsteps; ++s) {
     {
-      GPROF_T0
       wait_quads(s + 1);  // planes 4s-1 .. 4s+4
-      GPROF_ADD(5)
     }
-    GPROF_T0
     const int k = 4 * s + delta;
     const double fv = f_next;
     if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
@@ -508,25 +488,18 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
       wb[sm.po[k]] = gs_node_value<OP>(A, B, Cw, k, uu, fv);
     }
-    GPROF_ADD(6)
     // every 3 steps: all warps done with quads <= s-1 (the next step reads planes >= 4s+3);
     // refill them: quads up to s-1+NQ (the next three steps need quads <= s+4).
     if (s % 3 == 2 || s == nsteps - 1) {
-      GPROF_T0
       __syncthreads();
-      GPROF_ADD(7)
       const int to = min(s - 1 + NQ, last_quad);
       {
-        GPROF_T0
         issue_quads(next_quad, to);
-        GPROF_ADD(2)
       }
       next_quad = max(next_quad, to + 1);
     }
   }
-  GPROF_T0
   wait_quads(last_quad);  // every issued quad is consumed before the barriers are re-initialised
-  GPROF_ADD(9)
 }
 
 // thread 0: fresh quad barriers for the next colour pass (every thread is past
@@ -596,9 +569,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   MarchSmem<RING> sm(smem, slot_len, N);
   __shared__ int s_item;
   const int64_t total = ntl * n_bands;
-#ifdef HHG_GS_PROF
-  if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)(-clock64()));
-#endif
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -615,14 +585,11 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     Column q;
     double A[15], B[15];
     {
-      GPROF_T0
       band_setup<OP, RING>(sm, N, b, T, slot_len, coef10, cons, q, A, B);
-      GPROF_ADD(4)
     }
     constexpr bool kQuad = RING % 8 == 0 && RING >= 24;
     if (kQuad) gs_quad_bars_init(sm);  // visible after the pass-start bar.sync
     for (int colour = 0; colour < 4; ++colour) {
-      GPROF_T0
       if (threadIdx.x == 0 && colour > 0) {
         for (int bb = band - 1; bb <= band + 1; bb += 2) {
           if (bb < 0 || bb >= n_bands) continue;
@@ -640,20 +607,15 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
       // neighbours' generic global writes before their async-proxy reads
       if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
-      GPROF_ADD(0)
       {
-        GPROF_T0
         if (kQuad)
           gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
                                      u + T * S + q.c, Cw, false);
         else
           gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
         {
-          GPROF_T0
           __syncthreads();
-          GPROF_ADD(10)
         }
-        GPROF_ADD(1)
       }
       // bar.sync orders every thread's stores before thread 0's gpu-scope
       // release (cumulative); the neighbours' acquire loads pair with it
@@ -661,9 +623,6 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       if (kQuad && colour < 3) gs_quad_bars_init(sm);
     }
   }
-#ifdef HHG_GS_PROF
-  if (threadIdx.x == 0) atomicAdd(&g_gsprof[3], (unsigned long long)clock64());
-#endif
 }
 
 }  // namespace hhg

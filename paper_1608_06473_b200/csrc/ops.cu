@@ -912,12 +912,4 @@ extern "C" hhg_status hhg_profile_read(hhg_ctx ctx, int kind, double* total_ms, 
   return HHG_OK;
 }
 
-#ifdef HHG_GS_PROF
-extern "C" int hhg_gs_prof_read(unsigned long long* out) {
-  cudaMemcpyFromSymbol(out, hhg::g_gsprof, 12 * sizeof(unsigned long long));
-  unsigned long long z[12] = {0};
-  cudaMemcpyToSymbol(hhg::g_gsprof, z, sizeof(z));
-  return 0;
-}
-#endif
 
