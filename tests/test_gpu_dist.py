@@ -257,3 +257,19 @@ def test_results_bitwise_identical_across_rank_counts(part):
             assert np.all(np.abs(o["hist"] - ref["hist"]) <= 1e-12 * ref["hist"]), (world, o["hist"], ref["hist"])
             rel = np.linalg.norm(o["uv"] - ref["uv"]) / np.linalg.norm(ref["uv"])
             assert rel < 1e-12, (world, rel)
+
+
+@pytest.mark.parametrize("env", [{"HHG_OVERLAP": "0"}, {"HHG_GS_KERNEL": "wide4"}, {"HHG_GS_KERNEL": "passes"}])
+def test_rank_results_independent_of_overlap_and_gs_kernel(env, monkeypatch):
+    """The exchange/compute overlap (on by default) and the choice of volume GS
+    kernel do not change a single bit: 2 ranks with the overlap off, or with the
+    single-pass wavefront / the colour-pass kernels, reproduce the 1-rank
+    default vectors exactly."""
+    mesh_args, L = (0, 2), 4
+    ref = _run(1, mesh_args, L, "rcb")[0]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    res = _run(2, mesh_args, L, "rcb")
+    for r in range(2):
+        for name in ("y", "r", "ug"):
+            assert np.array_equal(res[r][name], ref[name]), (env, r, name)
