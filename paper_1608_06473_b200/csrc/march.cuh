@@ -127,12 +127,11 @@ __device__ __forceinline__ double rcp_nr(double x) {
 // x + k (y + k z) over three accumulation chains; shared by every GS kernel
 // (colour passes and the wavefront, gsfront.cuh), so their sweeps are bit-identical.
 // uu[15]: neighbour values in direction order (entry kMC unused).
-template <int OP>
-__device__ __forceinline__ double gs_node_value(const double (&A)[15], const double (&B)[15],
-                                                const double* __restrict__ Cw, int k, const double (&uu)[15],
-                                                double fv) {
+template <int OP, class CW>
+__device__ __forceinline__ double gs_node_value_acc(const double (&A)[15], const double (&B)[15], CW Cw, int k,
+                                                    const double (&uu)[15], double fv) {
   const double kd = (double)k;
-  const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(Cw[kMC], kd, B[kMC]), kd, A[kMC]) : A[kMC];
+  const double smc = (OP == HHG_OP_SURROGATE) ? fma(fma(Cw(kMC), kd, B[kMC]), kd, A[kMC]) : A[kMC];
   const double rinv = rcp_nr(smc);
   double r;
   if (OP == HHG_OP_SURROGATE) {
@@ -142,7 +141,7 @@ __device__ __forceinline__ double gs_node_value(const double (&A)[15], const dou
       if (w == kMC) continue;
       x = fma(A[w], uu[w], x);
       y = fma(B[w], uu[w], y);
-      z = fma(Cw[w], uu[w], z);
+      z = fma(Cw(w), uu[w], z);
     }
     r = fma(fma(z, kd, y), kd, x);
   } else {
@@ -155,6 +154,13 @@ __device__ __forceinline__ double gs_node_value(const double (&A)[15], const dou
     r = (acc[0] + acc[1]) + acc[2];
   }
   return (fv - r) * rinv;
+}
+
+template <int OP>
+__device__ __forceinline__ double gs_node_value(const double (&A)[15], const double (&B)[15],
+                                                const double* __restrict__ Cw, int k, const double (&uu)[15],
+                                                double fv) {
+  return gs_node_value_acc<OP>(A, B, [&](int w) { return Cw[w]; }, k, uu, fv);
 }
 
 // Shared-memory carve-up common to the march kernels (RING plane slots).
@@ -421,12 +427,11 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
 // slots of 4 planes whose bulk copies complete on one barrier (arrival count
 // 4: one arrive.expect_tx per plane, plain arrives past the last plane), so a
 // thread waits once per step (4 planes) instead of four times.
-template <int OP, int RING>
+template <int OP, int RING, class CW>
 __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_len, int N, const Band& b,
                                                  const Column& q, const double (&A)[15], const double (&B)[15],
                                                  int colour, double* __restrict__ ub, const double* __restrict__ fb,
-                                                 double* __restrict__ wb, const double* __restrict__ Cw,
-                                                 bool init_bars = true) {
+                                                 double* __restrict__ wb, CW Cw, bool init_bars = true) {
   constexpr int NQ = RING / 4;
   if (init_bars) {  // else the caller initialised them (gs_quad_bars_init) before a CTA barrier
     if (threadIdx.x == 0) {
@@ -486,7 +491,7 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
       const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
                              Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
                              Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
-      wb[sm.po[k]] = gs_node_value<OP>(A, B, Cw, k, uu, fv);
+      wb[sm.po[k]] = gs_node_value_acc<OP>(A, B, Cw, k, uu, fv);
     }
     // every 3 steps: all warps done with quads <= s-1 (the next step reads planes >= 4s+3);
     // refill them: quads up to s-1+NQ (the next three steps need quads <= s+4).
@@ -559,7 +564,10 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // while the grid has more CTAs than a macro has bands.
 // ---------------------------------------------------------------------------
 // Items come from an atomic counter; C_w through shared memory.
-template <int OP, int NT, int RING>
+// CWC: the macro's C_w from the constant bank g_cC (chunk [T0, T0 + ntl),
+// ntl <= kCMax, uploaded by the launcher) as uniform-register DFMA operands
+// (the item index is made warp-uniform by a shuffle); else from shared memory.
+template <int OP, int NT, int RING, bool CWC>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
@@ -608,9 +616,14 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       // neighbours' generic global writes before their async-proxy reads
       if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
       {
-        if (kQuad)
+        if (kQuad && CWC) {
+          const int cwb = __shfl_sync(0xffffffffu, (int)Tr, 0) * 15;
           gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
-                                     u + T * S + q.c, Cw, false);
+                                     u + T * S + q.c, [&](int w) { return g_cC[cwb + w]; }, false);
+        } else if (kQuad) {
+          gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
+                                     u + T * S + q.c, [&](int w) { return Cw[w]; }, false);
+        }
         else
           gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
         {

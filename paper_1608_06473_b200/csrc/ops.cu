@@ -344,8 +344,12 @@ static int gs_stress() {
 // The whole volume GS (4 colours) as one persistent launch (march.cuh::k_gs_items).
 template <int OP, int RING>
 static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* f, int64_t Tb, int64_t Te) {
+  // HHG_GS_CW=smem: C_w from shared memory; default: the constant bank (surrogate op)
+  const char* ce = getenv("HHG_GS_CW");
+  const bool cwc = OP == HHG_OP_SURROGATE && !(ce && std::string(ce) == "smem");
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N, RING);
-  const void* fn = (const void*)k_gs_items<OP, kMarchThreads, RING>;
+  const void* fn = cwc ? (const void*)k_gs_items<OP, kMarchThreads, RING, true>
+                       : (const void*)k_gs_items<OP, kMarchThreads, RING, false>;
   hhg_status st = smem_attr(c, fn);
   if (st != HHG_OK) return st;
   int grid = 0;
@@ -355,19 +359,27 @@ static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* 
   // resident at once (an item waits on its neighbour bands): otherwise use the
   // colour-pass kernels (no cross-CTA waits)
   if (grid <= nb) return HHG_ERR_STATE;
+  if (Te <= Tb) return HHG_OK;
+  if (cwc && (st = ensure_cC(c, lv, OP)) != HHG_OK) return st;
   // completion flags cleared per sweep (epoch 1): the launch is replayable from
   // a CUDA graph (hhg_vcycle)
-  const int64_t ntr = Te - Tb;
-  if (ntr <= 0) return HHG_OK;
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags + Tb * nb * 4, 0, (size_t)ntr * nb * 4 * sizeof(int), c->stream));
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags + Tb * nb * 4, 0, (size_t)(Te - Tb) * nb * 4 * sizeof(int), c->stream));
   lv.gs_epoch = 1;
-  HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
-  const int64_t items = ntr * nb;
   ProfScope ps(c, 1);
-  k_gs_items<OP, kMarchThreads, RING><<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
-      lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, ntr, Tb, lv.d_gs_counter,
-      lv.d_gs_flags, lv.gs_epoch, gs_stress());
-  HHG_LAUNCHED(c);
+  // macro chunks of <= kCMax (the constant-bank C_w table), run in order
+  for (int64_t T0 = Tb; T0 < Te; T0 += (cwc ? kCMax : Te - Tb)) {
+    const int64_t ntr = std::min<int64_t>(cwc ? kCMax : Te - Tb, Te - T0);
+    if (cwc)
+      HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, ntr * 15 * sizeof(double), 0,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+    HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
+    const int64_t items = ntr * nb;
+    auto kern = cwc ? k_gs_items<OP, kMarchThreads, RING, true> : k_gs_items<OP, kMarchThreads, RING, false>;
+    kern<<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
+        lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, ntr, T0, lv.d_gs_counter,
+        lv.d_gs_flags, lv.gs_epoch, gs_stress());
+    HHG_LAUNCHED(c);
+  }
   return HHG_OK;
 }
 
