@@ -267,10 +267,6 @@ constexpr int kResidUnroll = HHG_RESID_UNROLL;
 #define HHG_APPLY_UNROLL 1
 #endif
 constexpr int kApplyUnroll = HHG_APPLY_UNROLL;
-#ifndef HHG_GS_UNROLL
-#define HHG_GS_UNROLL 3
-#endif
-constexpr int kGsUnroll = HHG_GS_UNROLL;
 __constant__ double g_cC[kCMax * 15];
 
 template <int OP, int MODE>
@@ -423,28 +419,42 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
   }
 }
 
-// Same colour pass with QUAD mbarriers: the ring of RING planes is RING/4
-// slots of 4 planes whose bulk copies complete on one barrier (arrival count
-// 4: one arrive.expect_tx per plane, plain arrives past the last plane), so a
-// thread waits once per step (4 planes) instead of four times.
+// mbarrier wait on a precomputed shared-window address
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// GS colour pass of the persistent sweep (k_gs_items) with QUAD mbarriers: the
+// ring of RING planes is RING/4 slots of 4 planes whose bulk copies complete
+// on one barrier (arrival count 4: one arrive.expect_tx per plane, plain
+// arrives past the last plane), so a thread waits once per step of 4 planes;
+// the slot / phase of the next quad advance by one per step.  The 7 neighbour
+// columns of column c on diagonal d are c, c +- 1, c - d, c - d - 1,
+// c + d + 1, c + d + 2 (col(i,j) = d(d+1)/2 + j), so a plane needs three base
+// addresses and immediate offsets.  Refill every R = RING/4 - 3 steps behind a
+// CTA barrier; f is loaded FPD steps ahead.  The arithmetic per node is
+// gs_node_value_acc's, shared with every GS kernel (bit-identical sweeps).
+// The caller initialises the quad barriers (gs_quad_bars_init) before the
+// pass-start CTA barrier.
 template <int OP, int RING, class CW>
-__device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_len, int N, const Band& b,
-                                                 const Column& q, const double (&A)[15], const double (&B)[15],
-                                                 int colour, double* __restrict__ ub, const double* __restrict__ fb,
-                                                 double* __restrict__ wb, CW Cw, bool init_bars = true) {
+__device__ __forceinline__ void gs_colour_pass_t(MarchSmem<RING>& sm, int slot_len, const Band& b, const Column& q,
+                                                 const double (&A)[15], const double (&B)[15], int colour,
+                                                 double* __restrict__ ub, const double* __restrict__ fb,
+                                                 double* __restrict__ wb, CW Cw) {
   constexpr int NQ = RING / 4;
-  if (init_bars) {  // else the caller initialised them (gs_quad_bars_init) before a CTA barrier
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < NQ; ++s) mbar_init(&sm.bars[s], 4);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-  }
+  constexpr int R = NQ - 3;  // refill period (steps)
+  constexpr int FPD = 2;  // f loaded 2 steps ahead
   const int delta = (3 * ((((colour - q.d - q.j) % 4) + 4) % 4)) % 4;
   const int last_plane = b.kmax + 1;
   const int last_quad = last_plane / 4;
-  const int clo = b.c_lo;
-  // warp 0: issue quads [q0, q1] (lane = plane within the group)
   auto issue_quads = [&](int q0, int q1) {
     if (threadIdx.x < 32 && q1 >= q0) {
       for (int p = 4 * q0 + (int)threadIdx.x; p <= 4 * q1 + 3; p += 32) {
@@ -464,47 +474,63 @@ __device__ __forceinline__ void gs_colour_pass_q(MarchSmem<RING>& sm, int slot_l
   };
   int next_quad = min(NQ, last_quad + 1);
   issue_quads(0, next_quad - 1);
-  auto sptr = [&](int p) -> const double* { return sm.ring + sm.roff[p]; };
-  int waited = -1;
-  auto wait_quads = [&](int qq) {
-    qq = min(qq, last_quad);
-    for (; waited < qq;) {
-      ++waited;
-      mbar_wait(&sm.bars[waited % NQ], (waited / NQ) & 1);
+  const uint32_t bar0 = smem_u32(sm.bars);
+  int wslot = 0;
+  uint32_t wph = 0;
+  auto wait_next = [&]() {
+    mbar_wait_a(bar0 + 8u * (uint32_t)wslot, wph);
+    if (++wslot == NQ) {
+      wslot = 0;
+      wph ^= 1u;
     }
   };
+  wait_next();  // quad 0
+  const double* const rc = sm.ring + q.o_c;
+  const int d1 = q.d + 1;
+  const unsigned lenu = q.active ? (unsigned)q.len : 0u;  // node k exists iff (unsigned)(k - 1) < lenu
   const int nsteps = (b.kmax + 4) / 4;
-  double f_next = 0.0;
-  if (q.active && delta >= 1 && delta <= q.len) f_next = __ldg(fb + sm.po[delta]);
-#pragma unroll(kGsUnroll)
+  double fq[FPD];
+#pragma unroll
+  for (int x = 0; x < FPD; ++x) {
+    const int kk = 4 * x + delta;
+    fq[x] = ((unsigned)(kk - 1) < lenu) ? __ldg(fb + (unsigned)sm.po[kk]) : 0.0;
+  }
+  int cd = R;  // steps to the next refill
+#pragma unroll(R)
   for (int s = 0; s < nsteps; ++s) {
-    {
-      wait_quads(s + 1);  // planes 4s-1 .. 4s+4
-    }
+    if (s + 1 <= last_quad) wait_next();  // quad s+1: planes 4s-1 .. 4s+4 are in
     const int k = 4 * s + delta;
-    const double fv = f_next;
-    if (q.active && k + 4 >= 1 && k + 4 <= q.len) f_next = __ldg(fb + sm.po[k + 4]);
-    if (q.active && k >= 1 && k <= q.len) {
-      const double* Pb = sptr(k - 1);
-      const double* Pm = sptr(k);
-      const double* Pt = sptr(k + 1);
-      const double uu[15] = {Pb[q.o_c],  Pb[q.o_e],  Pb[q.o_n],  Pb[q.o_nw], Pm[q.o_s],
-                             Pm[q.o_se], Pm[q.o_w],  0.0,        Pm[q.o_e],  Pm[q.o_nw],
-                             Pm[q.o_n],  Pt[q.o_se], Pt[q.o_s],  Pt[q.o_w],  Pt[q.o_c]};
-      wb[sm.po[k]] = gs_node_value_acc<OP>(A, B, Cw, k, uu, fv);
+    const double fv = fq[0];
+#pragma unroll
+    for (int x = 0; x + 1 < FPD; ++x) fq[x] = fq[x + 1];
+    {
+      const int kf = k + 4 * FPD;
+      fq[FPD - 1] = ((unsigned)(kf - 1) < lenu) ? __ldg(fb + (unsigned)sm.po[kf]) : 0.0;
     }
-    // every 3 steps: all warps done with quads <= s-1 (the next step reads planes >= 4s+3);
-    // refill them: quads up to s-1+NQ (the next three steps need quads <= s+4).
-    if (s % 3 == 2 || s == nsteps - 1) {
+    if ((unsigned)(k - 1) < lenu) {
+      const double* Pb = rc + sm.roff[k - 1];
+      const double* Pm = rc + sm.roff[k];
+      const double* Pt = rc + sm.roff[k + 1];
+      const double* Pbh = Pb + d1;  // (i+1, j) (i, j+1)
+      const double* Pmh = Pm + d1;
+      const double* Pml = Pm - d1;  // (i, j-1) (i-1, j)
+      const double* Ptl = Pt - d1;
+      const double uu[15] = {Pb[0],  Pbh[0], Pbh[1], Pb[1],  Pml[0], Pm[-1], Pml[1], 0.0,
+                             Pmh[0], Pm[1],  Pmh[1], Pt[-1], Ptl[0], Ptl[1], Pt[0]};
+      wb[(unsigned)sm.po[k]] = gs_node_value_acc<OP>(A, B, Cw, k, uu, fv);
+    }
+    // every R steps: all warps done with quads <= s-1 (the next step reads planes >= 4s+3);
+    // refill them: quads up to s-1+NQ (the next R steps need quads <= s+R+1).
+    if (--cd == 0 || s == nsteps - 1) {
+      cd = R;
       __syncthreads();
       const int to = min(s - 1 + NQ, last_quad);
-      {
-        issue_quads(next_quad, to);
-      }
+      issue_quads(next_quad, to);
       next_quad = max(next_quad, to + 1);
     }
   }
-  wait_quads(last_quad);  // every issued quad is consumed before the barriers are re-initialised
+  // every issued quad is consumed before the barriers are re-initialised
+  for (int qq = min(nsteps, last_quad) + 1; qq <= last_quad; ++qq) wait_next();
 }
 
 // thread 0: fresh quad barriers for the next colour pass (every thread is past
@@ -567,16 +593,29 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
 // CWC: the macro's C_w from the constant bank g_cC (chunk [T0, T0 + ntl),
 // ntl <= kCMax, uploaded by the launcher) as uniform-register DFMA operands
 // (the item index is made warp-uniform by a shuffle); else from shared memory.
-template <int OP, int NT, int RING, bool CWC>
+template <int OP, int NT, int RING, bool CWC, bool PROF>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_gs_items(int N, int64_t S, const Band* __restrict__ bands, int n_bands, int slot_len,
                const double* __restrict__ coef10, const double* __restrict__ cons, double* __restrict__ u,
                const double* __restrict__ f, int64_t ntl, int64_t T0, int* __restrict__ counter,
-               int* __restrict__ flags, int epoch, int stress) {
+               int* __restrict__ flags, int epoch, int stress, unsigned long long* __restrict__ prof) {
+  static_assert(RING % 8 == 0 && RING >= 16, "quad ring: RING / 4 slots, refill period RING / 4 - 3 >= 1");
   extern __shared__ __align__(16) double smem[];
   MarchSmem<RING> sm(smem, slot_len, N);
   __shared__ int s_item;
   const int64_t total = ntl * n_bands;
+  // optional cycle accounting (PROF, tools/gsprof.py): thread 0's
+  // cycles in [0] item fetch + band setup, [1] flag wait, [2] pass-start
+  // barrier, [3] colour pass, [4] pass-end barrier; [6] steps, [7] items
+  long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tq = PROF ? clock64() : 0;
+  auto tick = [&](int slot, long long& t) {
+    if (PROF) {
+      const long long now = clock64();
+      pacc[slot] += now - t;
+      t = now;
+    }
+  };
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
@@ -588,15 +627,13 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     // stress test (HHG_GS_STRESS): bands of a macro handed out in reverse order
     // (macro-major order kept: still deadlock-free) and random delays below
     const int band = (stress & 1) ? n_bands - 1 - (int)(item - Tr * n_bands) : (int)(item - Tr * n_bands);
-    const double* const Cw = sm.Cw;
     const Band b = bands[band];
     Column q;
     double A[15], B[15];
-    {
-      band_setup<OP, RING>(sm, N, b, T, slot_len, coef10, cons, q, A, B);
-    }
-    constexpr bool kQuad = RING % 8 == 0 && RING >= 24;
-    if (kQuad) gs_quad_bars_init(sm);  // visible after the pass-start bar.sync
+    band_setup<OP, RING>(sm, N, b, T, slot_len, coef10, cons, q, A, B);
+    gs_quad_bars_init(sm);  // visible after the pass-start bar.sync
+    tick(0, tq);
+    pacc[7] += 1;
     for (int colour = 0; colour < 4; ++colour) {
       if (threadIdx.x == 0 && colour > 0) {
         for (int bb = band - 1; bb <= band + 1; bb += 2) {
@@ -611,31 +648,33 @@ __global__ void __launch_bounds__(NT, 512 / NT)
         }
       }
       if (stress && threadIdx.x == 0) __nanosleep(stress_hash(stress, (uint32_t)(T * n_bands + band), colour) & 8191);
+      tick(1, tq);
       __syncthreads();
+      tick(2, tq);
       // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
       // neighbours' generic global writes before their async-proxy reads
       if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
-      {
-        if (kQuad && CWC) {
-          const int cwb = __shfl_sync(0xffffffffu, (int)Tr, 0) * 15;
-          gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
-                                     u + T * S + q.c, [&](int w) { return g_cC[cwb + w]; }, false);
-        } else if (kQuad) {
-          gs_colour_pass_q<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c,
-                                     u + T * S + q.c, [&](int w) { return Cw[w]; }, false);
-        }
-        else
-          gs_colour_pass<OP, RING>(sm, slot_len, N, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c);
-        {
-          __syncthreads();
-        }
+      if (CWC) {
+        const int cwb = __shfl_sync(0xffffffffu, (int)Tr, 0) * 15;
+        gs_colour_pass_t<OP, RING>(sm, slot_len, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c,
+                                   [&](int w) { return g_cC[cwb + w]; });
+      } else {
+        const double* const Cw = sm.Cw;
+        gs_colour_pass_t<OP, RING>(sm, slot_len, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c,
+                                   [&](int w) { return Cw[w]; });
       }
+      tick(3, tq);
+      pacc[6] += (b.kmax + 4) / 4;
+      __syncthreads();
+      tick(4, tq);
       // bar.sync orders every thread's stores before thread 0's gpu-scope
       // release (cumulative); the neighbours' acquire loads pair with it
       if (threadIdx.x == 0) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
-      if (kQuad && colour < 3) gs_quad_bars_init(sm);
+      if (colour < 3) gs_quad_bars_init(sm);
     }
   }
+  if (PROF && threadIdx.x == 0)
+    for (int x = 0; x < 8; ++x) atomicAdd(prof + x, (unsigned long long)pacc[x]);
 }
 
 }  // namespace hhg

@@ -344,16 +344,21 @@ static int gs_stress() {
 // The whole volume GS (4 colours) as one persistent launch (march.cuh::k_gs_items).
 template <int OP, int RING>
 static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* f, int64_t Tb, int64_t Te) {
+  constexpr int NT = kMarchThreads;
   // HHG_GS_CW=smem: C_w from shared memory; default: the constant bank (surrogate op)
   const char* ce = getenv("HHG_GS_CW");
   const bool cwc = OP == HHG_OP_SURROGATE && !(ce && std::string(ce) == "smem");
+  // cycle accounting (hhg_gs_prof enabled): the instrumented instantiation
+  const bool prof = cwc && c->d_gsprof != nullptr;
   const size_t smem = march_smem_bytes(lv.slot_len, lv.N, RING);
-  const void* fn = cwc ? (const void*)k_gs_items<OP, kMarchThreads, RING, true>
-                       : (const void*)k_gs_items<OP, kMarchThreads, RING, false>;
+  if (smem > (size_t)kMaxDynSmem) return HHG_ERR_STATE;
+  auto kern = prof ? k_gs_items<OP, NT, RING, true, true>
+                   : cwc ? k_gs_items<OP, NT, RING, true, false> : k_gs_items<OP, NT, RING, false, false>;
+  const void* fn = (const void*)kern;
   hhg_status st = smem_attr(c, fn);
   if (st != HHG_OK) return st;
   int grid = 0;
-  if ((st = resident_grid(c, fn, kMarchThreads, smem, grid)) != HHG_OK) return st;
+  if ((st = resident_grid(c, fn, NT, smem, grid)) != HHG_OK) return st;
   const int nb = (int)lv.bands.size();
   // deadlock freedom needs every band of the partially handed-out macro
   // resident at once (an item waits on its neighbour bands): otherwise use the
@@ -374,10 +379,9 @@ static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* 
                                         cudaMemcpyDeviceToDevice, c->stream));
     HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
     const int64_t items = ntr * nb;
-    auto kern = cwc ? k_gs_items<OP, kMarchThreads, RING, true> : k_gs_items<OP, kMarchThreads, RING, false>;
-    kern<<<(unsigned)std::min<int64_t>(grid, items), kMarchThreads, smem, c->stream>>>(
+    kern<<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
         lv.N, lv.S, lv.d_bands, nb, lv.slot_len, lv.d_coef10, lv.d_cons, u, f, ntr, T0, lv.d_gs_counter,
-        lv.d_gs_flags, lv.gs_epoch, gs_stress());
+        lv.d_gs_flags, lv.gs_epoch, gs_stress(), c->d_gsprof);
     HHG_LAUNCHED(c);
   }
   return HHG_OK;

@@ -41,6 +41,17 @@ def main():
     torch.cuda.synchronize()
     c = ctx.gs_prof(True, read=True).astype(np.float64)
     ctx.gs_prof(False)
+    if os.environ.get("KB_ITEMS"):  # default k_gs_items sweep (instrumented instantiation): thread 0's cycles per phase
+        tag = os.environ.get("KB_TAG", "items")
+        items, steps = c[7] / reps, c[6] / reps
+        print(f"{tag}: {e0.elapsed_time(e1) / reps:.3f} ms/sweep, items {items:.0f}, passes {4 * items:.0f}, "
+              f"steps/pass {steps / max(4 * items, 1):.1f}")
+        names = ["item fetch+setup", "flag wait", "start bar.sync", "pass march", "end bar.sync"]
+        tot = sum(c[x] for x in range(5))
+        for x, n in enumerate(names):
+            print(f"   {n:17s} {c[x] / reps / max(4 * items, 1):9.0f} cyc/pass  {100 * c[x] / max(tot, 1):5.1f} %")
+        ctx.close()
+        return
     steps = c[6]
     names = ["plane wait", "node update", "halo wait", "progress", "barrier", "post-barrier"]
     tot = c[:6].sum()
