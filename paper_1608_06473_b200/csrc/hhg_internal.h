@@ -174,6 +174,10 @@ struct Level {
   std::vector<Band> bands_w;       // <= 2 kMarchThreads columns (single-pass GS, gsfront.cuh)
   Band* d_bands_w = nullptr;
   int slot_len_w = 0;
+  // bands of the producer-warp GS (gsprod.cuh): <= 224 / 480 columns (7 / 15 compute warps)
+  std::vector<Band> bands_p[2];
+  Band* d_bands_p[2] = {nullptr, nullptr};
+  int slot_len_p[2] = {0, 0};
   std::vector<Band> bands_fem;  // element-wise FEM: <= kMarchThreads anchor columns per band
   Band* d_bands_fem = nullptr;
   // structured face rows (faces.cu): row r = face * nfi + q, q in colour-major order

@@ -57,6 +57,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// mbarrier wait on a precomputed shared-window address
+__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
 // Delays of the protocol stress tests (HHG_GS_STRESS): a 32-bit hash.
 __device__ __forceinline__ uint32_t stress_hash(uint32_t seed, uint32_t a, uint32_t b) {
   uint32_t h = seed * 0x9e3779b9u ^ (a + 0x7f4a7c15u) * 0x85ebca6bu ^ (b + 0x165667b1u) * 0xc2b2ae35u;
@@ -419,19 +432,6 @@ __device__ __forceinline__ void gs_colour_pass(MarchSmem<RING>& sm, int slot_len
   }
 }
 
-// mbarrier wait on a precomputed shared-window address
-__device__ __forceinline__ void mbar_wait_a(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-
 // GS colour pass of the persistent sweep (k_gs_items) with QUAD mbarriers: the
 // ring of RING planes is RING/4 slots of 4 planes whose bulk copies complete
 // on one barrier (arrival count 4: one arrive.expect_tx per plane, plain
@@ -667,9 +667,10 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       pacc[6] += (b.kmax + 4) / 4;
       __syncthreads();
       tick(4, tq);
-      // bar.sync orders every thread's stores before thread 0's gpu-scope
-      // release (cumulative); the neighbours' acquire loads pair with it
-      if (threadIdx.x == 0) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
+      // bar.sync orders every thread's stores before the gpu-scope release
+      // (cumulative); the neighbours' acquire loads pair with it
+      // (by warp 1: its fence overlaps thread 0's poll of the next pass's flags)
+      if (threadIdx.x == 32) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
       if (colour < 3) gs_quad_bars_init(sm);
     }
   }

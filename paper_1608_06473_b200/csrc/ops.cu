@@ -13,6 +13,7 @@
 #include "vol_kernels.cuh"
 #include "march.cuh"
 #include "gsfront.cuh"
+#include "gsprod.cuh"
 #include "gslex.cuh"
 #include "femew.cuh"
 
@@ -387,6 +388,46 @@ static hhg_status launch_gs_items_r(Ctx* c, Level& lv, double* u, const double* 
   return HHG_OK;
 }
 
+// The persistent 4-colour sweep with a producer warp and per-plane
+// cross-band progress (gsprod.cuh; HHG_GS_KERNEL=prod: 7 compute warps, two
+// CTAs per SM; prodw: 15 compute warps, one CTA per SM).
+template <int OP, int RING, int NCW>
+static hhg_status launch_gs_prod(Ctx* c, Level& lv, double* u, const double* f, int64_t Tb, int64_t Te) {
+  constexpr int NT = 32 * NCW + 32;
+  const int x = NCW <= 7 ? 0 : 1;
+  if (lv.bands_p[x].empty()) return HHG_ERR_STATE;
+  const bool cwc = OP == HHG_OP_SURROGATE;
+  const size_t smem = march_smem_bytes(lv.slot_len_p[x], lv.N, RING);
+  if (smem > (size_t)(NCW <= 7 ? 113 * 1024 : kMaxDynSmem)) return HHG_ERR_STATE;
+  auto kern = cwc ? k_gs_prod<OP, RING, true, NCW> : k_gs_prod<OP, RING, false, NCW>;
+  const void* fn = (const void*)kern;
+  hhg_status st = smem_attr(c, fn);
+  if (st != HHG_OK) return st;
+  int grid = 0;
+  if ((st = resident_grid(c, fn, NT, smem, grid)) != HHG_OK) return st;
+  const int nb = (int)lv.bands_p[x].size();
+  if (grid <= nb) return HHG_ERR_STATE;  // every band of the partially handed-out macro resident
+  if ((size_t)nb > lv.bands.size() * 4) return HHG_ERR_STATE;  // progress words fit d_gs_flags
+  if (Te <= Tb) return HHG_OK;
+  if (cwc && (st = ensure_cC(c, lv, OP)) != HHG_OK) return st;
+  // progress words (one per (macro, band)) cleared per sweep: replayable from a CUDA graph
+  HHG_CK(c, cudaMemsetAsync(lv.d_gs_flags + Tb * nb, 0, (size_t)(Te - Tb) * nb * sizeof(int), c->stream));
+  ProfScope ps(c, 1);
+  for (int64_t T0 = Tb; T0 < Te; T0 += (cwc ? kCMax : Te - Tb)) {
+    const int64_t ntr = std::min<int64_t>(cwc ? kCMax : Te - Tb, Te - T0);
+    if (cwc)
+      HHG_CK(c, cudaMemcpyToSymbolAsync(g_cC, lv.d_cC + T0 * 15, ntr * 15 * sizeof(double), 0,
+                                        cudaMemcpyDeviceToDevice, c->stream));
+    HHG_CK(c, cudaMemsetAsync(lv.d_gs_counter, 0, sizeof(int), c->stream));
+    const int64_t items = ntr * nb;
+    kern<<<(unsigned)std::min<int64_t>(grid, items), NT, smem, c->stream>>>(
+        lv.N, lv.S, lv.d_bands_p[x], nb, lv.slot_len_p[x], lv.d_coef10, lv.d_cons, u, f, ntr, T0, lv.d_gs_counter,
+        lv.d_gs_flags, gs_stress());
+    HHG_LAUNCHED(c);
+  }
+  return HHG_OK;
+}
+
 template <int OP>
 static hhg_status launch_gs_items(Ctx* c, Level& lv, double* u, const double* f, int64_t Tb, int64_t Te) {
   // 24-plane ring only while two CTAs fit an SM (N = 256: 768-double slots -> 16)
@@ -652,17 +693,24 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
   // HHG_GS_KERNEL (read per call, so tests can compare the variants):
   // default = the persistent 4-pass sweep k_gs_items; the single-pass wavefront
   // k_gs_front as "front" (256 threads, LAG 4), "front6" (LAG 6), "wide4" /
-  // "wide6" (512 threads); "passes" = 4 colour launches
+  // "wide6" (512 threads); the producer-warp sweep k_gs_prod as "prod" (7
+  // compute warps) / "prodw" (15); "passes" = 4 colour launches
   const char* e = getenv("HHG_GS_KERNEL");
   const std::string ks = e ? e : "";
-  const int mode = ks == "passes" ? 1 : ks == "front" ? 3 : ks == "front6" ? 4 : ks == "wide4" ? 5 : ks == "wide6" ? 6 : 2;
+  const int mode = ks == "passes" ? 1 : ks == "front" ? 3 : ks == "front6" ? 4 : ks == "wide4" ? 5 : ks == "wide6" ? 6 : ks == "prod" ? 7 : ks == "prodw" ? 8 : 2;
   const bool march_ok = march_path(lv, op);
   auto sweep = [&](int64_t Tb, int64_t Te) -> hhg_status {
     hhg_status st = HHG_ERR_STATE;
     if (march_ok && mode == 2)
       st = op == HHG_OP_SURROGATE ? launch_gs_items<HHG_OP_SURROGATE>(c, lv, u, f, Tb, Te)
                                   : launch_gs_items<HHG_OP_CONST_AFFINE>(c, lv, u, f, Tb, Te);
-    if (march_ok && mode >= 3 && Tb == 0 && Te == c->nt_local) {
+    if (march_ok && mode == 7)
+      st = op == HHG_OP_SURROGATE ? launch_gs_prod<HHG_OP_SURROGATE, 24, 7>(c, lv, u, f, Tb, Te)
+                                  : launch_gs_prod<HHG_OP_CONST_AFFINE, 24, 7>(c, lv, u, f, Tb, Te);
+    if (march_ok && mode == 8)
+      st = op == HHG_OP_SURROGATE ? launch_gs_prod<HHG_OP_SURROGATE, 32, 15>(c, lv, u, f, Tb, Te)
+                                  : launch_gs_prod<HHG_OP_CONST_AFFINE, 32, 15>(c, lv, u, f, Tb, Te);
+    if (march_ok && mode >= 3 && mode <= 6 && Tb == 0 && Te == c->nt_local) {
       const int variant = mode - 3;
       st = op == HHG_OP_SURROGATE ? launch_gs_front<HHG_OP_SURROGATE>(c, lv, u, f, variant)
                                   : launch_gs_front<HHG_OP_CONST_AFFINE>(c, lv, u, f, variant);
@@ -677,7 +725,7 @@ hhg_status gs_sweep_dev(Ctx* c, Level& lv, int op, double* u, const double* f, b
   };
   // multi-rank: the ghost exchange of the swept volume values overlaps the
   // sweep of the interior macros (HHG_OVERLAP=0 disables)
-  if (c->nranks > 1 && march_ok && (mode == 1 || mode == 2) && overlap_on()) {
+  if (c->nranks > 1 && march_ok && (mode == 1 || mode == 2 || mode >= 7) && overlap_on()) {
     hhg_status st = sweep(0, c->nt_bnd);
     if (st != HHG_OK) return st;
     return dist_sync_overlapped(c, lv, u, [&]() { return sweep(c->nt_bnd, c->nt_local); });

@@ -244,6 +244,9 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   // wide bands (<= 2 kMarchThreads columns) of the single-pass GS (gsfront.cuh)
   if (!make_bands(2 * kMarchThreads, lv.bands_w, lv.slot_len_w))
     return set_err(c, HHG_ERR_INVALID, "diagonal longer than a CTA");
+  // producer-warp GS bands (7 / 15 compute warps); empty if a diagonal does not fit
+  for (int x = 0; x < 2; ++x)
+    if (!make_bands(x ? 480 : 224, lv.bands_p[x], lv.slot_len_p[x])) lv.bands_p[x].clear();
   // element-wise FEM bands: <= kMarchThreads ANCHOR columns (every column of a
   // diagonal, d+1; the first band also anchors diagonal 1's 2 columns)
   lv.bands_fem.clear();
@@ -588,6 +591,8 @@ static hhg_status build_level(Ctx* c, Topology& tp, int L) {
   if ((st = up(lv.d_dir_gid, dgid)) != HHG_OK) return st;
   if ((st = up(lv.d_bands, lv.bands)) != HHG_OK) return st;
   if ((st = up(lv.d_bands_w, lv.bands_w)) != HHG_OK) return st;
+  for (int x = 0; x < 2; ++x)
+    if (!lv.bands_p[x].empty() && (st = up(lv.d_bands_p[x], lv.bands_p[x])) != HHG_OK) return st;
   if ((st = up(lv.d_bands_fem, lv.bands_fem)) != HHG_OK) return st;
   {
     const size_t nfl = (size_t)c->nt_local * std::max<size_t>(lv.bands.size(), 1) * 4;
@@ -618,7 +623,7 @@ static void free_level(Level& lv) {
                 lv.d_row_gid, lv.d_dir_slot, lv.d_dir_gid, lv.d_tmp, lv.d_coef, lv.d_cons,
                 lv.d_coef10, lv.d_bands, lv.d_gs_flags, lv.d_gs_counter,
                 lv.d_flp, lv.d_fst, lv.d_fcidx, lv.d_fval, lv.d_fval_cons, lv.d_ftmp, lv.d_po,
-                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red, lv.d_fne[0], lv.d_fne[1], lv.d_fne[2], lv.d_gs_ex, lv.d_gs_prog, lv.d_gs_epoch, lv.d_bands_w};
+                lv.d_send_slot, lv.d_recv_slot, lv.d_sendbuf, lv.d_recvbuf, lv.d_cC, lv.d_rsum_ptr, lv.d_rsum_slot, lv.d_rsum_idx, lv.d_ew_lo, lv.d_ew_hi, lv.d_bands_fem, lv.d_fcoef, lv.d_cg_rp, lv.d_cg_col, lv.d_cg_val, lv.d_cg_vec, lv.d_cg_part, lv.d_cg_red, lv.d_fne[0], lv.d_fne[1], lv.d_fne[2], lv.d_gs_ex, lv.d_gs_prog, lv.d_gs_epoch, lv.d_bands_w, lv.d_bands_p[0], lv.d_bands_p[1]};
   for (void* p : ps)
     if (p) cudaFree(p);
   lv = Level();

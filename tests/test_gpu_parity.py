@@ -449,11 +449,12 @@ def test_non_positive_centre_weight_raises_numeric():
     ctx.close()
 
 
-@pytest.mark.parametrize("kernel", ["front", "front6", "wide4", "wide6", "default"])
+@pytest.mark.parametrize("kernel", ["front", "front6", "wide4", "wide6", "prod", "prodw", "default"])
 @pytest.mark.parametrize("mesh_name,L", [("tet", 7), ("shell480", 5), ("shell60", 4), ("tet", 3)])
 def test_gs_kernels_bit_identical(mesh_name, L, kernel, monkeypatch):
     """Every volume GS kernel -- the persistent 4-pass sweep (default), the
-    single-pass wavefronts ("front", "front6", "wide4", "wide6") and the 4
+    single-pass wavefronts ("front", "front6", "wide4", "wide6"), the
+    producer-warp sweeps with per-plane progress ("prod", "prodw") and the 4
     colour launches ("passes", the reference here) -- computes the same
     4-colour sweep bit for bit (same per-node arithmetic gs_node_value, same
     colour order); surrogate and constant-stencil smoothers."""
@@ -492,13 +493,14 @@ def test_coarse_cg_through_operator_calls_matches_oracle(monkeypatch):
     assert rel(ctx.gather_global(4, du), u_ref) < 1e-10
 
 
-@pytest.mark.parametrize("kernel", ["default", "front", "wide4"])
+@pytest.mark.parametrize("kernel", ["default", "front", "wide4", "prod", "prodw"])
 @pytest.mark.parametrize("seed", [1, 2, 3])
 @pytest.mark.parametrize("mesh_name,L", [("tet", 7), ("shell480", 5)])
 def test_gs_flag_protocol_stress(mesh_name, L, seed, kernel, monkeypatch):
     """Stress of the cross-CTA protocols of the persistent GS kernels
     (completion flags of the 4-pass sweep; LL halo words and progress words of
-    the wavefront, PAPER.md:1306-1315 update order): bands of every macro
+    the wavefront; per-plane progress words of the producer-warp sweeps,
+    PAPER.md:1306-1315 update order): bands of every macro
     handed out in reverse order (odd seeds) and random delays of up to ~8 us
     before passes / steps -- the sweep stays bit-identical to the 4 colour
     launches, which have no cross-CTA waits at all."""
