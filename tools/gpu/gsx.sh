@@ -1,3 +1,2 @@
-for v in preord nomid; do for k in prod prodw; do
-  KB_LIB=tools/variants/libhhg_$v.so HHG_GS_KERNEL=$k KB_OPS=gs KB_TAG=$v-$k KB_CHECK=1 timeout 120 python tools/kbench.py 1 2 7 10 >> gpurun_out/gsx.log 2>&1
-done; done
+timeout 1200 python -m pytest tests/test_gpu_dist.py -q -x > gpurun_out/gsx_tests.log 2>&1
+echo "rc=$?" >> gpurun_out/gsx_tests.log
