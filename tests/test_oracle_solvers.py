@@ -213,3 +213,31 @@ def test_lexicographic_gs_is_forward_substitution(shell3):
     x = np.zeros(num.n_total)
     x[unk] = spla.spsolve(A[unk][:, unk].tocsc(), f[unk])
     assert np.abs(gs.sweep_lex(x.copy(), f, 1) - x).max() <= 1e-10 * np.abs(x).max()
+
+
+@pytest.mark.parametrize("L", [1, 2, 3])
+def test_class_step_schedule_vertex_exchange_can_ride_with_edge_colour_0(L):
+    """The lattice fact behind the library's 6-exchange GS sweep
+    (ops.cu::gs_sweep_dev skips the exchange after the vertex step): in the
+    assembled FEM matrix no edge row of colour 0 (even positions m >= 2) has a
+    vertex column, and an edge row of colour 1 reads edge-colour-0 nodes of
+    its OWN edge only -- so the vertex values may travel with the edge-colour-0
+    exchange, while edge colour 1 still needs it."""
+    mesh = synth.shell_mesh(0.55, 1.0, 0, 2)
+    N = 2 ** L
+    num = G.Numbering(mesh, N)
+    A = fem.assemble(mesh, N, num).tocsr()
+    saw_vertex_in_colour1 = False
+    for g in range(num.base_e, num.base_f):
+        if num.dirichlet_mask[g]:
+            continue
+        eid, m0 = divmod(g - num.base_e, N - 1)
+        cols = A.indices[A.indptr[g]:A.indptr[g + 1]]
+        if (m0 + 1) % 2 == 0:
+            assert not np.any(cols < num.base_e), (g, cols[cols < num.base_e])
+        else:
+            saw_vertex_in_colour1 |= bool(np.any(cols < num.base_e))
+            ec = cols[(cols >= num.base_e) & (cols < num.base_f)]
+            other = ec[(ec - num.base_e) // (N - 1) != eid]
+            assert all(num.step_of(int(x)) != 1 for x in other), (g, other)  # step 1 = edge colour 0
+    assert saw_vertex_in_colour1 == (N >= 2)
