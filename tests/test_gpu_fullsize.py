@@ -231,3 +231,35 @@ def test_fullsize_fem_operator_sampled(t, nr, L):
         ref = float(np.dot(sw, un))
         scale = float(np.abs(sw * un).sum())
         assert abs(out["yfem"][gI] - ref) <= TOL * scale, (T, i, j, k, out["yfem"][gI], ref)
+
+
+@pytest.mark.parametrize("kernel", ["default", "prodw", "wide4"])
+def test_fullsize_gs_kernels_bit_identical(kernel, monkeypatch):
+    """At the bench size (480-macro shell, L = 7, 167 M unknowns, the launch
+    configuration bench.py times), two GS sweeps of the persistent kernels are
+    bit-identical to the 4 colour launches (HHG_GS_KERNEL=passes), which have
+    no cross-CTA waits at all."""
+    import torch
+
+    import paper_1608_06473_b200 as hhg
+    L = 7
+    mesh = synth.shell_mesh(0.55, 1.0, 1, 2)
+    ctx = hhg.Ctx.from_mesh(mesh, L)
+    ctx.fit(2, "lsqp", 2)
+    n_local, n_owned, n_global = ctx.layout(L)
+    g = np.arange(n_global)
+    u, f = ctx.zeros(L), ctx.zeros(L)
+    ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(0, g)).cuda(), u)
+    ctx.scatter_global(L, torch.from_numpy(synth.uniform_pm1(1, g)).cuda(), f)
+    del g
+    ref = u.clone()
+    monkeypatch.setenv("HHG_GS_KERNEL", "passes")
+    ctx.gs_sweep(L, ref, f, 2)
+    if kernel == "default":
+        monkeypatch.delenv("HHG_GS_KERNEL")
+    else:
+        monkeypatch.setenv("HHG_GS_KERNEL", kernel)
+    ctx.gs_sweep(L, u, f, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(u, ref)
+    ctx.close()
