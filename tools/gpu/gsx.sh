@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_fullsize.py -q -x -k "kernels_bit_identical" > gpurun_out/gsx_tests.log 2>&1
-echo "rc=$?" >> gpurun_out/gsx_tests.log
+for v in base nof base nof; do
+  KB_LIB=tools/variants/libhhg_$v.so KB_OPS=gs KB_TAG=$v timeout 120 python tools/kbench.py 1 2 7 10 >> gpurun_out/gsx.log 2>&1
+done
