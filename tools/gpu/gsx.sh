@@ -1,3 +1,3 @@
-for v in base nof base nof; do
-  KB_LIB=tools/variants/libhhg_$v.so KB_OPS=gs KB_TAG=$v timeout 120 python tools/kbench.py 1 2 7 10 >> gpurun_out/gsx.log 2>&1
+for v in base r2 r1 base r2 r1; do
+  KB_LIB=tools/variants/libhhg_$v.so KB_OPS=gs KB_TAG=$v KB_CHECK=1 timeout 120 python tools/kbench.py 1 2 7 10 >> gpurun_out/gsx.log 2>&1
 done
