@@ -233,17 +233,18 @@ def test_fullsize_fem_operator_sampled(t, nr, L):
         assert abs(out["yfem"][gI] - ref) <= TOL * scale, (T, i, j, k, out["yfem"][gI], ref)
 
 
-@pytest.mark.parametrize("kernel", ["default", "prodw", "wide4"])
-def test_fullsize_gs_kernels_bit_identical(kernel, monkeypatch):
+@pytest.mark.parametrize("t,nr,L,kernel", [(1, 2, 7, "default"), (1, 2, 7, "prodw"), (1, 2, 7, "wide4"),
+                                           (None, None, 8, "default")])
+def test_fullsize_gs_kernels_bit_identical(t, nr, L, kernel, monkeypatch):
     """At the bench size (480-macro shell, L = 7, 167 M unknowns, the launch
-    configuration bench.py times), two GS sweeps of the persistent kernels are
-    bit-identical to the 4 colour launches (HHG_GS_KERNEL=passes), which have
-    no cross-CTA waits at all."""
+    configuration bench.py times) and on the widest lattice the ABI accepts
+    (single tet, L = 8: the 16-plane ring, refill every step), two GS sweeps
+    of the persistent kernels are bit-identical to the 4 colour launches
+    (HHG_GS_KERNEL=passes), which have no cross-CTA waits at all."""
     import torch
 
     import paper_1608_06473_b200 as hhg
-    L = 7
-    mesh = synth.shell_mesh(0.55, 1.0, 1, 2)
+    mesh = _mesh(t, nr)
     ctx = hhg.Ctx.from_mesh(mesh, L)
     ctx.fit(2, "lsqp", 2)
     n_local, n_owned, n_global = ctx.layout(L)
