@@ -320,7 +320,7 @@ __global__ void __launch_bounds__(kMarchThreads, 2)
   double* const optr = out + T * S + q.c;
   const double* const fptr = f + T * S + q.c;
   // residual: f is loaded FPD steps ahead (its HBM latency hides behind them)
-  constexpr int FPD = 3;
+  constexpr int FPD = 5;  // (3: 1.451 ms, 5: 1.440, 8: spills, 1.586)
   double fq[FPD];
 #pragma unroll
   for (int x = 0; x < FPD; ++x)
