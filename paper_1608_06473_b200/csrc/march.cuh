@@ -448,7 +448,7 @@ template <int OP, int RING, class CW>
 __device__ __forceinline__ void gs_colour_pass_t(MarchSmem<RING>& sm, int slot_len, const Band& b, const Column& q,
                                                  const double (&A)[15], const double (&B)[15], int colour,
                                                  double* __restrict__ ub, const double* __restrict__ fb,
-                                                 double* __restrict__ wb, CW Cw) {
+                                                 double* __restrict__ wb, CW Cw, bool pre_issued = false) {
   constexpr int NQ = RING / 4;
   constexpr int R = NQ - 3;  // refill period (steps)
   constexpr int FPD = 2;  // f loaded 2 steps ahead
@@ -473,7 +473,7 @@ __device__ __forceinline__ void gs_colour_pass_t(MarchSmem<RING>& sm, int slot_l
     }
   };
   int next_quad = min(NQ, last_quad + 1);
-  issue_quads(0, next_quad - 1);
+  if (!pre_issued) issue_quads(0, next_quad - 1);  // else gs_issue_first did
   const uint32_t bar0 = smem_u32(sm.bars);
   int wslot = 0;
   uint32_t wph = 0;
@@ -533,6 +533,31 @@ __device__ __forceinline__ void gs_colour_pass_t(MarchSmem<RING>& sm, int slot_l
   for (int qq = min(nsteps, last_quad) + 1; qq <= last_quad; ++qq) wait_next();
 }
 
+// Warp 0: the first RING/4 quads of a band's colour pass (= gs_colour_pass_t's
+// own first issue), for a caller that puts them in flight early.
+template <int RING>
+__device__ __forceinline__ void gs_issue_first(MarchSmem<RING>& sm, int slot_len, const Band& b,
+                                               const double* __restrict__ ub) {
+  constexpr int NQ = RING / 4;
+  const int last_plane = b.kmax + 1;
+  const int q1 = min(NQ, last_plane / 4 + 1) - 1;
+  if (threadIdx.x < 32) {
+    for (int p = (int)threadIdx.x; p <= 4 * q1 + 3; p += 32) {
+      uint64_t* bar = &sm.bars[(p >> 2) % NQ];
+      if (p <= last_plane) {
+        const int g0 = sm.po[p] + b.c_lo;
+        const int a0 = g0 & ~1;
+        const int a1 = (g0 + b.ncols + 1) & ~1;
+        const uint32_t bytes = (uint32_t)((a1 - a0) * 8);
+        mbar_expect_tx(bar, bytes);
+        tma_load_1d(sm.ring + (p % RING) * slot_len, ub + a0, bytes, bar);
+      } else {
+        mbar_arrive(bar);
+      }
+    }
+  }
+}
+
 // thread 0: fresh quad barriers for the next colour pass (every thread is past
 // the previous pass's last wait); made visible by the caller's next bar.sync
 template <int RING>
@@ -541,6 +566,20 @@ __device__ __forceinline__ void gs_quad_bars_init(MarchSmem<RING>& sm) {
     for (int s = 0; s < RING / 4; ++s) mbar_init(&sm.bars[s], 4);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+}
+
+// Shared-memory tables of a band (plane offsets, ring offsets, C_w), then a
+// CTA barrier.
+template <int OP, int RING>
+__device__ __forceinline__ void band_tables(MarchSmem<RING>& sm, int N, const Band& b, int64_t T, int slot_len,
+                                            const double* __restrict__ coef10) {
+  if (threadIdx.x < 15) sm.Cw[threadIdx.x] = (OP == HHG_OP_SURROGATE) ? coef10[T * 150 + threadIdx.x * 10 + 9] : 0.0;
+  for (int p = threadIdx.x; p <= N + 1; p += blockDim.x) {
+    const int pof = (int)plane_off(N, p);
+    sm.po[p] = pof;
+    sm.roff[p] = (p % RING) * slot_len + ((pof + b.c_lo) & 1);
+  }
+  __syncthreads();
 }
 
 template <int OP, int RING = kRing>
@@ -619,8 +658,7 @@ __global__ void __launch_bounds__(NT, 512 / NT)
   for (;;) {
     if (threadIdx.x == 0) s_item = atomicAdd(counter, 1);
     __syncthreads();
-    const int64_t item = s_item;
-    __syncthreads();
+    const int64_t item = s_item;  // rewritten only after band_tables' CTA barrier
     if (item >= total) break;
     const int64_t Tr = item / n_bands;  // macro within the launch's range [T0, T0 + ntl)
     const int64_t T = T0 + Tr;
@@ -630,8 +668,15 @@ __global__ void __launch_bounds__(NT, 512 / NT)
     const Band b = bands[band];
     Column q;
     double A[15], B[15];
-    band_setup<OP, RING>(sm, N, b, T, slot_len, coef10, cons, q, A, B);
-    gs_quad_bars_init(sm);  // visible after the pass-start bar.sync
+    // tables, then colour 0's first quads go in flight (colour 0 waits for no
+    // neighbour), then the column coefficients: their L2 latency overlaps the
+    // bulk copies
+    gs_quad_bars_init(sm);  // visible after band_tables' CTA barrier
+    band_tables<OP, RING>(sm, N, b, T, slot_len, coef10);
+    if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
+    gs_issue_first<RING>(sm, slot_len, b, u + T * S);
+    q = make_column(b, N);
+    column_coeffs<OP>(coef10, cons, T, q.i, q.j, A, B);
     tick(0, tq);
     pacc[7] += 1;
     for (int colour = 0; colour < 4; ++colour) {
@@ -649,19 +694,21 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       }
       if (stress && threadIdx.x == 0) __nanosleep(stress_hash(stress, (uint32_t)(T * n_bands + band), colour) & 8191);
       tick(1, tq);
-      __syncthreads();
+      if (colour > 0) {
+        __syncthreads();
+        // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
+        // neighbours' generic global writes before their async-proxy reads
+        if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
       tick(2, tq);
-      // the lanes of warp 0 issue the pass's bulk copies: order this CTA's and the
-      // neighbours' generic global writes before their async-proxy reads
-      if (threadIdx.x < 32) asm volatile("fence.proxy.async.global;" ::: "memory");
       if (CWC) {
         const int cwb = __shfl_sync(0xffffffffu, (int)Tr, 0) * 15;
         gs_colour_pass_t<OP, RING>(sm, slot_len, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c,
-                                   [&](int w) { return g_cC[cwb + w]; });
+                                   [&](int w) { return g_cC[cwb + w]; }, colour == 0);
       } else {
         const double* const Cw = sm.Cw;
         gs_colour_pass_t<OP, RING>(sm, slot_len, b, q, A, B, colour, u + T * S, f + T * S + q.c, u + T * S + q.c,
-                                   [&](int w) { return Cw[w]; });
+                                   [&](int w) { return Cw[w]; }, colour == 0);
       }
       tick(3, tq);
       pacc[6] += (b.kmax + 4) / 4;
