@@ -716,8 +716,9 @@ __global__ void __launch_bounds__(NT, 512 / NT)
       tick(4, tq);
       // bar.sync orders every thread's stores before the gpu-scope release
       // (cumulative); the neighbours' acquire loads pair with it
-      // (by warp 1: its fence overlaps thread 0's poll of the next pass's flags)
-      if (threadIdx.x == 32) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
+      // (by warp 1: its fence overlaps thread 0's poll of the next pass's
+      // flags; colour 3's flag is never awaited, so it is not released)
+      if (threadIdx.x == 32 && colour < 3) st_release_gpu(flags + ((T * n_bands + band) * 4 + colour), epoch);
       if (colour < 3) gs_quad_bars_init(sm);
     }
   }
