@@ -484,17 +484,17 @@ __device__ __forceinline__ void gs_colour_pass_t(MarchSmem<RING>& sm, int slot_l
       wph ^= 1u;
     }
   };
-  wait_next();  // quad 0
   const double* const rc = sm.ring + q.o_c;
   const int d1 = q.d + 1;
   const unsigned lenu = q.active ? (unsigned)q.len : 0u;  // node k exists iff (unsigned)(k - 1) < lenu
   const int nsteps = (b.kmax + 4) / 4;
-  double fq[FPD];
+  double fq[FPD];  // (issued before the first quad wait: the latencies overlap)
 #pragma unroll
   for (int x = 0; x < FPD; ++x) {
     const int kk = 4 * x + delta;
     fq[x] = ((unsigned)(kk - 1) < lenu) ? __ldg(fb + (unsigned)sm.po[kk]) : 0.0;
   }
+  wait_next();  // quad 0
   int cd = R;  // steps to the next refill
 #pragma unroll(R)
   for (int s = 0; s < nsteps; ++s) {
