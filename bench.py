@@ -135,7 +135,9 @@ def oracle_sample(L, q, n_macros=1):
     t2 = np.vectorize(remap.get)(tets)
     mesh = synth.MacroMesh(sh.vertices[vids], sh.radius[vids], t2, np.ones_like(t2, dtype=np.uint8))
     num = G.Numbering(mesh, 2 ** L)
+    t_setup = time.perf_counter()
     Lt, _, _ = S.surrogate_operator(mesh, L, q, num=num)
+    oracle_sample.setup_s = time.perf_counter() - t_setup  # FEM sampling + LSQP fit + CSR assembly
     gs = solvers.GS(Lt, num)
     g = np.arange(num.n_total)
     u = synth.uniform_pm1(0, g) * num.unknown_mask
@@ -606,7 +608,12 @@ def cpu_baseline(L, q):
             ts.append(time.perf_counter() - t0)
         t = statistics.median(ts)
         out = {"value": 2 * n_unk / t / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": sample + f", {len(ts)} reps, median"}
+               "sample": sample + f", {len(ts)} reps, median",
+               # the oracle's setup of the sample macro (FEM node
+               # sampling, LSQP fit, CSR assembly of its operator) next to the
+               # library's whole setup (config.setup_s: mesh, lattice, fit of
+               # every macro; PAPER.md:1205-1214 Table setup)
+               "setup_s_per_macro": round(getattr(oracle_sample, "setup_s", float("nan")), 2)}
         out["all_cores"] = cpu_baseline_parallel(step, n_unk, sample)
         return out
     except Exception as e:  # pragma: no cover
